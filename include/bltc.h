@@ -1,0 +1,175 @@
+/*
+ * bltc.h -- C ABI of libbltc, the B200-native (sm_100a) BLTC evaluation path.
+ *
+ * Drop-in boundary: the reference exposes the path as Python functions
+ *   bltc.engine.treecode_potentials(system, config, threads)   engine.py:350-372
+ *   bltc.decomp.run_distributed(system, config, ranks, threads) decomp.py:483-593
+ * plus the stage functions its tests call directly
+ *   build_source_tree / build_target_batches                    tree.py:191-253
+ *   build_interaction_lists / lists_against_root / count_pairs   engine.py:110-143
+ *   compute_all_moments                                          moments.py:147-150
+ *   compute_potentials                                           engine.py:315-335
+ * The Python shim (paper_2003_01836_b200/engine.py, decomp.py) keeps those
+ * signatures and binds the entry points below through ctypes; see
+ * INTEGRATION.md for the binding a reference maintainer would add.
+ *
+ * Conventions: plain pointers and sizes, no torch types.  Every function
+ * returns BLTC_OK (0) or a negative status; bltc_last_error() gives a
+ * thread-local message.  Host-pointer arguments are borrowed for the call;
+ * device-pointer arguments must live on the context's device.  A context
+ * owns its device buffers and one CUDA stream; it is not thread-safe (one
+ * context per host thread and device).  No C++ exception crosses this ABI.
+ */
+#ifndef BLTC_H
+#define BLTC_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define BLTC_API __attribute__((visibility("default")))
+#else
+#define BLTC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BLTC_OK 0
+#define BLTC_ERR_VALUE -1      /* maps to ValueError (engine.py:56-62, kernels.py:49-51, tree.py:182) */
+#define BLTC_ERR_CUDA -2       /* CUDA runtime / launch failure */
+#define BLTC_ERR_STATE -3      /* stage export without a preceding run */
+#define BLTC_ERR_UNSUPPORTED -4
+
+/* Evaluation modes.
+ * PARITY: bit-faithful to the reference (IEEE sqrt/div, no FMA, the
+ *         reference's per-target accumulation order incl. Neumaier).
+ * FAST:   rsqrt + FMA, register-blocked tiles, load-balanced work items;
+ *         validated against PARITY / the oracle within tolerances. */
+#define BLTC_MODE_PARITY 0
+#define BLTC_MODE_FAST 1
+
+typedef struct bltc_ctx bltc_ctx;
+
+/* EvalConfig (engine.py:46-62) + KernelSpec (kernels.py:42-55) + mode. */
+typedef struct {
+  double theta;          /* MAC parameter, (0, 1] */
+  int32_t degree;        /* interpolation degree n >= 0 */
+  int32_t kernel_code;   /* 0 Coulomb, 1 Yukawa, 2 test constant (kernels.py:39) */
+  int64_t leaf_size;     /* N_L >= 1 */
+  int64_t batch_size;    /* N_B >= 1 */
+  double kappa;          /* Yukawa screening, finite >= 0 */
+  int32_t mode;          /* BLTC_MODE_* */
+  int32_t all_moments;   /* 1: moments for every eligible cluster (compute_all_moments);
+                            0: only clusters that some approximation list reads */
+} bltc_params;
+
+/* RunStats (engine.py:338-347) plus device-side detail.  Times are CUDA-event
+ * times on the context stream, in seconds. */
+typedef struct {
+  int64_t n_clusters;
+  int64_t n_batches;
+  int64_t direct_pairs;
+  int64_t approx_pairs;
+  double setup_s;        /* tree + batches + lists */
+  double precompute_s;   /* moments */
+  double compute_s;      /* evaluation + un-permute */
+  double total_s;        /* setup + precompute + compute (device) */
+  double h2d_s;          /* host->device copies (host-pointer entry points) */
+  double d2h_s;
+  double far_s;          /* far-field kernel time (FAST mode: separate kernel) */
+  double near_s;         /* near-field kernel time */
+  int64_t n_moments;     /* clusters whose moments were computed */
+  int64_t kernel_launches;
+  int32_t tree_depth;
+  int32_t batch_depth;
+} bltc_stats;
+
+BLTC_API const char* bltc_last_error(void);
+BLTC_API const char* bltc_version(void);
+
+/* device < 0: current device.  stream: a cudaStream_t to run on, or NULL for
+ * a context-owned non-blocking stream. */
+BLTC_API int bltc_create(int device, void* stream, bltc_ctx** out);
+BLTC_API int bltc_destroy(bltc_ctx* ctx);
+/* Non-zero: record per-phase CUDA events (needs stream syncs between phases). */
+BLTC_API int bltc_set_timing(bltc_ctx* ctx, int enable);
+
+/* treecode_potentials (engine.py:350-372) on HOST buffers: copies inputs H2D
+ * (pinned host memory is used as such), runs tree/batches/lists/moments/
+ * evaluation on the device and copies phi (original target order) D2H.
+ * coincident != 0 means targets are the sources (ParticleSystem.coincident,
+ * particles.py:62-64); then t* may equal s* and are not read separately. */
+BLTC_API int bltc_treecode(bltc_ctx* ctx, const bltc_params* p, const double* cheb_s, int64_t n_t,
+                  const double* tx, const double* ty, const double* tz, int64_t n_s,
+                  const double* sx, const double* sy, const double* sz, const double* q,
+                  int32_t coincident, double* phi_out, bltc_stats* stats);
+
+/* Same on DEVICE buffers (inputs resident in HBM; phi_out device pointer). */
+BLTC_API int bltc_treecode_device(bltc_ctx* ctx, const bltc_params* p, const double* cheb_s, int64_t n_t,
+                         const double* tx, const double* ty, const double* tz, int64_t n_s,
+                         const double* sx, const double* sy, const double* sz,
+                         const double* q, int32_t coincident, double* phi_out,
+                         bltc_stats* stats);
+
+/* ---- Stage introspection of the last run (bit-exact checks) ------------- */
+typedef struct {
+  int64_t n_sources, n_targets;
+  int64_t n_clusters, n_batches;
+  int64_t n_approx, n_direct;      /* CSR entries */
+  int64_t n_moments;
+  int32_t degree;
+  int32_t tree_depth, batch_depth;
+} bltc_sizes;
+
+BLTC_API int bltc_get_sizes(bltc_ctx* ctx, bltc_sizes* out);
+/* which: 0 source tree (clusters, BFS order), 1 target partition (all nodes).
+ * Arrays sized n_nodes (lo/hi: 3*n_nodes), perm sized n_particles.  Any
+ * pointer may be NULL. */
+BLTC_API int bltc_export_tree(bltc_ctx* ctx, int which, int64_t* n_nodes_out, int64_t* perm,
+                     int64_t* start, int64_t* stop, double* lo, double* hi,
+                     int64_t* child_start, int64_t* child_count, int32_t* level);
+/* Target batches in DFS (= ascending start) order. */
+BLTC_API int bltc_export_batches(bltc_ctx* ctx, int64_t* start, int64_t* stop, double* center,
+                        double* radius);
+/* Interaction lists, CSR over batches: ptr sized n_batches+1. */
+BLTC_API int bltc_export_lists(bltc_ctx* ctx, int64_t* a_ptr, int64_t* a_idx, int64_t* d_ptr,
+                      int64_t* d_idx);
+/* Moments: cluster ids [n_moments] and rows [n_moments][(n+1)^3]. */
+BLTC_API int bltc_export_moments(bltc_ctx* ctx, int64_t* cluster_ids, double* rows);
+
+/* ---- Distributed (one rank per GPU; decomp.py:483-593) ------------------
+ * Each rank: bltc_rank_build (local tree, batches, moments of every cluster
+ * that may be approximated) -> bltc_rank_publish_sizes / bltc_rank_publish
+ * (flattened TreeArray records, decomp.py:137-189, + particles + moment
+ * rows into caller-provided DEVICE buffers) -> the caller all-gathers those
+ * buffers (NCCL over NVLink) -> bltc_rank_evaluate against the gathered
+ * forest in the reference's owner order (local first, then remote owners
+ * ascending; decomp.py:437-454). */
+typedef struct {
+  int64_t n_clusters;
+  int64_t n_particles;
+  int64_t n_moment_rows;
+  int64_t record_doubles;   /* doubles per cluster record */
+} bltc_publish_sizes;
+
+BLTC_API int bltc_rank_build(bltc_ctx* ctx, const bltc_params* p, const double* cheb_s, int64_t n,
+                    const double* x, const double* y, const double* z, const double* q,
+                    int32_t device_ptrs);
+BLTC_API int bltc_rank_publish_sizes(bltc_ctx* ctx, bltc_publish_sizes* out);
+/* records: [n_clusters][record_doubles]; particles: [4][n_particles] (x,y,z,q);
+ * moments: [n_moment_rows][(n+1)^3].  All device pointers. */
+BLTC_API int bltc_rank_publish(bltc_ctx* ctx, double* records, double* particles, double* moments);
+/* Forest of R published trees (device pointers, one per owner rank, owner
+ * order 0..R-1); my_rank's own entry is the local tree.  phi_out: host (or
+ * device if device_ptrs) buffer in the rank's ORIGINAL particle order. */
+BLTC_API int bltc_rank_evaluate(bltc_ctx* ctx, const bltc_params* p, int32_t ranks, int32_t my_rank,
+                       const int64_t* n_clusters, const int64_t* n_particles,
+                       const int64_t* n_moment_rows, const double* const* records,
+                       const double* const* particles, const double* const* moments,
+                       double* phi_out, int32_t device_ptrs, bltc_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLTC_H */

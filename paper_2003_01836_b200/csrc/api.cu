@@ -1,0 +1,780 @@
+// libbltc C ABI (include/bltc.h): contexts, the single-device pipeline that
+// replaces treecode_potentials (engine.py:350-372), stage exports for the
+// bit-exact checks, and the per-rank entry points of the distributed path
+// (decomp.py:483-593).
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "bltc_internal.cuh"
+#include "eval_common.cuh"
+
+namespace bltc {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+__global__ void k_moments(const double* sx, const double* sy, const double* sz,
+                          const double* sq, const int32_t* list, const int32_t* cstart,
+                          const int32_t* cstop, const double* lo, const double* hi,
+                          const double* s_nodes, const double* w_nodes, int degree,
+                          double* rows);
+__global__ void k_lists(int64_t nb, int G, int g, const double* bcenter, const double* bradius,
+                        const int32_t* bstart, const int32_t* bstop, const MacNode* nodes,
+                        int32_t cluster_offset, double theta, int64_t per_node, bool fill,
+                        int32_t* a_cnt, int32_t* d_cnt, const int32_t* a_ptr,
+                        const int32_t* d_ptr, int32_t* a_idx, int32_t* d_idx,
+                        unsigned long long* pairs, int32_t* overflow);
+__global__ void k_mark_used(int64_t n, const int32_t* idx, int32_t* used);
+
+namespace {
+
+inline int grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  return (int)(g < 1 ? 1 : g);
+}
+
+// Derived cluster geometry (tree.py:46-53, 205-206): center = 0.5 (lo + hi),
+// radius = 0.5 sqrt((ex^2 + ey^2) + ez^2), eligible = all extents >= 1e-14.
+__global__ void k_mac_nodes(int64_t nn, const double* lo, const double* hi, const int32_t* start,
+                            const int32_t* stop, const int32_t* child_start,
+                            const int32_t* child_count, MacNode* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  MacNode n;
+  double e[3], c[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    c[d] = __dmul_rn(0.5, __dadd_rn(lo[3 * i + d], hi[3 * i + d]));
+    e[d] = __dsub_rn(hi[3 * i + d], lo[3 * i + d]);
+  }
+  n.cx = c[0];
+  n.cy = c[1];
+  n.cz = c[2];
+  n.radius = __dmul_rn(
+      0.5, __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(e[0], e[0]), __dmul_rn(e[1], e[1])),
+                                __dmul_rn(e[2], e[2]))));
+  n.count = stop[i] - start[i];
+  n.child_count = child_count[i];
+  n.child_start = child_count[i] ? child_start[i] : -1;
+  n.eligible = (e[0] >= kDegenerate && e[1] >= kDegenerate && e[2] >= kDegenerate) ? 1 : 0;
+  out[i] = n;
+}
+
+__global__ void k_eval_clusters(int64_t nn, const double* lo, const double* hi,
+                                const int32_t* start, const int32_t* stop, int32_t offset,
+                                EvalCluster* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  EvalCluster c;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    c.lo[d] = lo[3 * i + d];
+    c.hi[d] = hi[3 * i + d];
+  }
+  c.start = start[i] + offset;
+  c.stop = stop[i] + offset;
+  c.mrow = -1;
+  c.pad = 0;
+  out[i] = c;
+}
+
+__global__ void k_batches(int64_t nb, const int32_t* leaves, const double* lo, const double* hi,
+                          const int32_t* start, const int32_t* stop, int32_t* bstart,
+                          int32_t* bstop, double* bc, double* br) {
+  int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  int i = leaves[b];
+  double e[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    bc[3 * b + d] = __dmul_rn(0.5, __dadd_rn(lo[3 * i + d], hi[3 * i + d]));
+    e[d] = __dsub_rn(hi[3 * i + d], lo[3 * i + d]);
+  }
+  br[b] = __dmul_rn(0.5, __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(e[0], e[0]),
+                                                        __dmul_rn(e[1], e[1])),
+                                              __dmul_rn(e[2], e[2]))));
+  bstart[b] = start[i];
+  bstop[b] = stop[i];
+}
+
+__global__ void k_flag_moments(int64_t nn, const MacNode* nodes, int64_t per_node, int all,
+                               const int32_t* used, int32_t* flag) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  int f;
+  if (all == 1) f = nodes[i].eligible;                                  // compute_all_moments
+  else if (all == 2) f = nodes[i].eligible && per_node < nodes[i].count;  // any possible approx
+  else f = used[i];
+  flag[i] = f;
+}
+
+__global__ void k_compact_moments(int64_t nn, const int32_t* flag, const int32_t* pos,
+                                  int32_t* list, EvalCluster* ecl) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  if (flag[i]) {
+    list[pos[i]] = (int32_t)i;
+    ecl[i].mrow = pos[i];
+  }
+}
+
+__global__ void k_pack4(int64_t n, const double* x, const double* y, const double* z,
+                        const double* q, double4* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = make_double4(x[i], y[i], z[i], q[i]);
+}
+
+__global__ void k_unpermute(int64_t n, const double* sorted, const int32_t* perm, double* phi) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) phi[i] = sorted[perm[i]];
+}
+
+__global__ void k_widen(int64_t n, const int32_t* a, int64_t* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = a[i];
+}
+
+}  // namespace
+}  // namespace bltc
+
+using namespace bltc;
+
+struct bltc_ctx {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  bool timing = true;
+  HostScratch hs;
+  BuildScratch bs;
+  Partition src, tgt_own;
+  Partition* tgt = nullptr;
+  DBuf<double> in[7];        // H2D staging: tx ty tz sx sy sz q
+  DBuf<MacNode> mac;
+  DBuf<EvalCluster> ecl;
+  DBuf<double> bcenter, bradius;
+  DBuf<int32_t> bstart, bstop;
+  Lists lists;
+  DBuf<int32_t> used, mflag, mpos, mlist;
+  DBuf<double> rows;
+  int64_t n_moments = 0;
+  DBuf<double> s_nodes, w_nodes;
+  DBuf<double> out_sorted, far_out, phi_dev;
+  DBuf<double4> src4;
+  DBuf<int32_t> flag;
+  DBuf<int64_t> widen;
+  bltc_params params{};
+  bool have_run = false;
+  int64_t launches = 0;
+  // distributed: per-rank forest
+  bool rank_built = false;
+  int64_t rank_n = 0;
+  DBuf<EvalCluster> f_ecl;
+  DBuf<MacNode> f_mac;
+  DBuf<double> f_x, f_y, f_z, f_q, f_rows;
+  DBuf<double4> f_src4;
+};
+
+namespace {
+
+void check_params(const bltc_params* p) {
+  if (!p) {
+    set_error("params is NULL");
+    throw UserError{BLTC_ERR_VALUE};
+  }
+  if (!(p->theta > 0.0 && p->theta <= 1.0)) {
+    set_error("theta must be in (0, 1], got " + std::to_string(p->theta));
+    throw UserError{BLTC_ERR_VALUE};
+  }
+  if (p->degree < 0) {
+    set_error("degree must be >= 0");
+    throw UserError{BLTC_ERR_VALUE};
+  }
+  if (p->degree > kMaxDegree) {
+    set_error("degree above the supported maximum " + std::to_string(kMaxDegree));
+    throw UserError{BLTC_ERR_UNSUPPORTED};
+  }
+  if (p->leaf_size < 1 || p->batch_size < 1) {
+    set_error("leaf_size and batch_size must be >= 1");
+    throw UserError{BLTC_ERR_VALUE};
+  }
+  if (!std::isfinite(p->kappa) || p->kappa < 0.0) {
+    set_error("kappa must be finite and >= 0, got " + std::to_string(p->kappa));
+    throw UserError{BLTC_ERR_VALUE};
+  }
+  if (p->kernel_code < 0 || p->kernel_code > 2) {
+    set_error("kernel_code must be 0, 1 or 2");
+    throw UserError{BLTC_ERR_VALUE};
+  }
+  if (p->mode != BLTC_MODE_PARITY && p->mode != BLTC_MODE_FAST) {
+    set_error("mode must be BLTC_MODE_PARITY or BLTC_MODE_FAST");
+    throw UserError{BLTC_ERR_VALUE};
+  }
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return BLTC_OK;
+  } catch (const UserError& e) {
+    return e.code;
+  } catch (const CudaFailure&) {
+    return BLTC_ERR_CUDA;
+  } catch (const std::exception& e) {
+    set_error(std::string("internal error: ") + e.what());
+    return BLTC_ERR_CUDA;
+  } catch (...) {
+    set_error("unknown internal error");
+    return BLTC_ERR_CUDA;
+  }
+}
+
+struct Timer {
+  cudaEvent_t ev[8];
+  int n = 0;
+  bool on;
+  cudaStream_t st;
+  Timer(bool enable, cudaStream_t s) : on(enable), st(s) {
+    if (on)
+      for (auto& e : ev) BLTC_CUDA(cudaEventCreate(&e));
+  }
+  ~Timer() {
+    if (on)
+      for (auto& e : ev) cudaEventDestroy(e);
+  }
+  void mark() {
+    if (on) BLTC_CUDA(cudaEventRecord(ev[n++], st));
+  }
+  double secs(int a, int b) {
+    if (!on) return 0.0;
+    BLTC_CUDA(cudaEventSynchronize(ev[b]));
+    float ms = 0;
+    BLTC_CUDA(cudaEventElapsedTime(&ms, ev[a], ev[b]));
+    return ms * 1e-3;
+  }
+};
+
+void upload_nodes(bltc_ctx* c, const bltc_params* p, const double* cheb_s) {
+  const int m = p->degree + 1;
+  std::vector<double> w(m);
+  for (int k = 0; k < m; ++k) {   // barycentric_weights (interp.py:59-67)
+    double delta = (k == 0 || k == p->degree) ? 0.5 : 1.0;
+    w[k] = (k % 2 == 0 ? 1.0 : -1.0) * delta;
+  }
+  if (p->degree == 0) w[0] = 0.5;
+  c->s_nodes.resize(m);
+  c->w_nodes.resize(m);
+  double* h = (double*)c->hs.get(2 * m * sizeof(double) + 64);
+  for (int k = 0; k < m; ++k) {
+    h[k] = cheb_s ? cheb_s[k] : 0.0;
+    h[m + k] = w[k];
+  }
+  BLTC_CUDA(cudaMemcpyAsync(c->s_nodes.p, h, m * sizeof(double), cudaMemcpyHostToDevice, c->st));
+  BLTC_CUDA(cudaMemcpyAsync(c->w_nodes.p, h + m, m * sizeof(double), cudaMemcpyHostToDevice,
+                            c->st));
+  BLTC_CUDA(cudaStreamSynchronize(c->st));
+}
+
+// Interaction lists of the target batches against one or more source trees
+// (groups), CSR batch-major then group.
+void build_lists(bltc_ctx* c, const bltc_params* p, int G, const MacNode* const* trees,
+                 const int32_t* cluster_offsets) {
+  cudaStream_t st = c->st;
+  Lists& L = c->lists;
+  const int64_t nb = c->bstart.n;
+  const int64_t nseg = nb * G;
+  const int64_t per_node = (int64_t)(p->degree + 1) * (p->degree + 1) * (p->degree + 1);
+  L.nb = nb;
+  L.n_groups = G;
+  L.a_cnt.resize(nseg + 1);
+  L.d_cnt.resize(nseg + 1);
+  L.a_ptr.resize(nseg + 1);
+  L.d_ptr.resize(nseg + 1);
+  L.pairs.resize(2);
+  c->flag.resize(1);
+  BLTC_CUDA(cudaMemsetAsync(L.pairs.p, 0, 2 * sizeof(unsigned long long), st));
+  BLTC_CUDA(cudaMemsetAsync(c->flag.p, 0, sizeof(int32_t), st));
+  BLTC_CUDA(cudaMemsetAsync(L.a_cnt.p + nseg, 0, sizeof(int32_t), st));
+  BLTC_CUDA(cudaMemsetAsync(L.d_cnt.p + nseg, 0, sizeof(int32_t), st));
+  for (int g = 0; g < G; ++g) {
+    k_lists<<<grid_for(nb, 64), 64, 0, st>>>(nb, G, g, c->bcenter.p, c->bradius.p, c->bstart.p,
+                                             c->bstop.p, trees[g], cluster_offsets[g], p->theta,
+                                             per_node, false, L.a_cnt.p, L.d_cnt.p, nullptr,
+                                             nullptr, nullptr, nullptr, L.pairs.p, c->flag.p);
+    BLTC_LAUNCH_CHECK();
+    ++c->launches;
+  }
+  exclusive_scan_i32(L.a_cnt.p, L.a_ptr.p, nseg + 1, c->bs.scan_tmp, st);
+  exclusive_scan_i32(L.d_cnt.p, L.d_ptr.p, nseg + 1, c->bs.scan_tmp, st);
+  int32_t* h = (int32_t*)c->hs.get(64);
+  BLTC_CUDA(cudaMemcpyAsync(h, L.a_ptr.p + nseg, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  BLTC_CUDA(cudaMemcpyAsync(h + 1, L.d_ptr.p + nseg, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  BLTC_CUDA(cudaMemcpyAsync(h + 2, c->flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  BLTC_CUDA(cudaStreamSynchronize(st));
+  if (h[2]) {
+    set_error("interaction-list traversal stack overflow (tree too deep)");
+    throw UserError{BLTC_ERR_UNSUPPORTED};
+  }
+  L.n_approx = h[0];
+  L.n_direct = h[1];
+  L.a_idx.resize(L.n_approx + 1);
+  L.d_idx.resize(L.n_direct + 1);
+  for (int g = 0; g < G; ++g) {
+    k_lists<<<grid_for(nb, 64), 64, 0, st>>>(nb, G, g, c->bcenter.p, c->bradius.p, c->bstart.p,
+                                             c->bstop.p, trees[g], cluster_offsets[g], p->theta,
+                                             per_node, true, nullptr, nullptr, L.a_ptr.p,
+                                             L.d_ptr.p, L.a_idx.p, L.d_idx.p, nullptr, c->flag.p);
+    BLTC_LAUNCH_CHECK();
+    ++c->launches;
+  }
+}
+
+// Moments of the flagged clusters of one source tree (moments.py:147-150).
+// all: 0 = clusters on some approximation list, 1 = every eligible cluster,
+// 2 = every cluster the MAC could accept (eligible and (n+1)^3 < N_C).
+void compute_moments(bltc_ctx* c, const bltc_params* p, const Partition& T, const MacNode* mac,
+                     EvalCluster* ecl, int all, DBuf<double>& rows, int64_t cluster_base) {
+  cudaStream_t st = c->st;
+  const int64_t nn = T.n_nodes;
+  const int m = p->degree + 1;
+  const int64_t m3 = (int64_t)m * m * m;
+  c->used.resize(nn);
+  c->mflag.resize(nn + 1);
+  c->mpos.resize(nn + 1);
+  if (all == 0) {
+    BLTC_CUDA(cudaMemsetAsync(c->used.p, 0, nn * sizeof(int32_t), st));
+    // approximation entries are global ids; this tree's ids start at cluster_base
+    if (c->lists.n_approx > 0) {
+      k_mark_used<<<grid_for(c->lists.n_approx, 256), 256, 0, st>>>(
+          c->lists.n_approx, c->lists.a_idx.p, c->used.p);
+      BLTC_LAUNCH_CHECK();
+      ++c->launches;
+    }
+  }
+  (void)cluster_base;
+  k_flag_moments<<<grid_for(nn, 256), 256, 0, st>>>(nn, mac, m3, all, c->used.p, c->mflag.p);
+  BLTC_LAUNCH_CHECK();
+  BLTC_CUDA(cudaMemsetAsync(c->mflag.p + nn, 0, sizeof(int32_t), st));
+  exclusive_scan_i32(c->mflag.p, c->mpos.p, nn + 1, c->bs.scan_tmp, st);
+  int32_t* h = (int32_t*)c->hs.get(64);
+  BLTC_CUDA(cudaMemcpyAsync(h, c->mpos.p + nn, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  BLTC_CUDA(cudaStreamSynchronize(st));
+  c->n_moments = h[0];
+  c->mlist.resize(c->n_moments + 1);
+  rows.resize(c->n_moments * m3 + 1);
+  k_compact_moments<<<grid_for(nn, 256), 256, 0, st>>>(nn, c->mflag.p, c->mpos.p, c->mlist.p,
+                                                       ecl);
+  BLTC_LAUNCH_CHECK();
+  c->launches += 3;
+  if (c->n_moments > 0) {
+    int threads = ((m * m + 31) / 32) * 32;
+    if (threads < 96) threads = 96;
+    k_moments<<<(unsigned)c->n_moments, threads, 0, st>>>(
+        T.x.p, T.y.p, T.z.p, T.q.p, c->mlist.p, T.start.p, T.stop.p, T.lo.p, T.hi.p,
+        c->s_nodes.p, c->w_nodes.p, p->degree, rows.p);
+    BLTC_LAUNCH_CHECK();
+    ++c->launches;
+  }
+}
+
+void build_batches(bltc_ctx* c, Partition& T) {
+  cudaStream_t st = c->st;
+  partition_leaves(T, c->bs, st, c->hs);
+  const int64_t nb = T.n_leaves;
+  c->bstart.resize(nb);
+  c->bstop.resize(nb);
+  c->bcenter.resize(3 * nb);
+  c->bradius.resize(nb);
+  k_batches<<<grid_for(nb, 128), 128, 0, st>>>(nb, T.leaves.p, T.lo.p, T.hi.p, T.start.p,
+                                               T.stop.p, c->bstart.p, c->bstop.p, c->bcenter.p,
+                                               c->bradius.p);
+  BLTC_LAUNCH_CHECK();
+  c->launches += 4;
+}
+
+void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, const double* sx,
+              const double* sy, const double* sz, const double* sq, const double4* src4,
+              const double* rows, bltc_stats* stats) {
+  cudaStream_t st = c->st;
+  const Partition& T = *c->tgt;
+  EvalArgs a{};
+  a.nb = c->bstart.n;
+  a.G = G;
+  a.bstart = c->bstart.p;
+  a.bstop = c->bstop.p;
+  a.tx = T.x.p;
+  a.ty = T.y.p;
+  a.tz = T.z.p;
+  a.a_ptr = c->lists.a_ptr.p;
+  a.a_idx = c->lists.a_idx.p;
+  a.d_ptr = c->lists.d_ptr.p;
+  a.d_idx = c->lists.d_idx.p;
+  a.clusters = ecl;
+  a.sx = sx;
+  a.sy = sy;
+  a.sz = sz;
+  a.sq = sq;
+  a.src4 = src4;
+  a.moments = rows;
+  a.s_nodes = c->s_nodes.p;
+  a.degree = p->degree;
+  a.kappa = p->kappa;
+  c->out_sorted.resize(T.n);
+  a.out = c->out_sorted.p;
+  a.work = nullptr;
+  if (p->mode == BLTC_MODE_PARITY) {
+    launch_eval_parity(a, p->kernel_code, st);
+    c->launches += 1;
+  } else {
+    c->far_out.resize(T.n);
+    a.far_out = c->far_out.p;
+    float far_ms = 0, near_ms = 0;
+    launch_eval_fast(a, p->kernel_code, st, st, nullptr, &far_ms, &near_ms, c->timing);
+    c->launches += 2;
+    if (stats) {
+      stats->far_s = far_ms * 1e-3;
+      stats->near_s = near_ms * 1e-3;
+    }
+  }
+}
+
+void run_pipeline(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64_t n_t,
+                  const double* tx, const double* ty, const double* tz, int64_t n_s,
+                  const double* sx, const double* sy, const double* sz, const double* q,
+                  bool coincident, double* phi_dev, bltc_stats* stats) {
+  check_params(p);
+  if (n_s < 1 || n_t < 1) {
+    set_error("cannot partition an empty particle set");
+    throw UserError{BLTC_ERR_VALUE};
+  }
+  if (n_s > (int64_t)INT32_MAX / 2 || n_t > (int64_t)INT32_MAX / 2) {
+    set_error("particle count above the supported 2^30 per device");
+    throw UserError{BLTC_ERR_UNSUPPORTED};
+  }
+  cudaStream_t st = c->st;
+  c->params = *p;
+  c->have_run = false;
+  c->launches = 0;
+  Timer tm(c->timing, st);
+  upload_nodes(c, p, cheb_s);
+  tm.mark();  // 0
+  // ---- setup: source tree, target batches, interaction lists
+  build_partition(c->src, c->bs, n_s, sx, sy, sz, q, p->leaf_size, st, c->hs);
+  const bool share = coincident && p->batch_size == p->leaf_size;
+  if (share) {
+    c->tgt = &c->src;   // identical inputs + limits => identical partition (tree.py:225-236)
+  } else {
+    build_partition(c->tgt_own, c->bs, n_t, coincident ? sx : tx, coincident ? sy : ty,
+                    coincident ? sz : tz, nullptr, p->batch_size, st, c->hs);
+    c->tgt = &c->tgt_own;
+  }
+  build_batches(c, *c->tgt);
+  const int64_t nn = c->src.n_nodes;
+  c->mac.resize(nn);
+  c->ecl.resize(nn);
+  k_mac_nodes<<<grid_for(nn, 128), 128, 0, st>>>(nn, c->src.lo.p, c->src.hi.p, c->src.start.p,
+                                                 c->src.stop.p, c->src.child_start.p,
+                                                 c->src.child_count.p, c->mac.p);
+  k_eval_clusters<<<grid_for(nn, 128), 128, 0, st>>>(nn, c->src.lo.p, c->src.hi.p,
+                                                     c->src.start.p, c->src.stop.p, 0, c->ecl.p);
+  BLTC_LAUNCH_CHECK();
+  const MacNode* trees[1] = {c->mac.p};
+  const int32_t offs[1] = {0};
+  build_lists(c, p, 1, trees, offs);
+  tm.mark();  // 1
+  // ---- precompute: moments
+  compute_moments(c, p, c->src, c->mac.p, c->ecl.p, p->all_moments ? 1 : 0, c->rows, 0);
+  tm.mark();  // 2
+  // ---- compute: evaluation + un-permute
+  if (p->mode == BLTC_MODE_FAST) {
+    c->src4.resize(n_s);
+    k_pack4<<<grid_for(n_s, 256), 256, 0, st>>>(n_s, c->src.x.p, c->src.y.p, c->src.z.p,
+                                                c->src.q.p, c->src4.p);
+    BLTC_LAUNCH_CHECK();
+    ++c->launches;
+  }
+  evaluate(c, p, 1, c->ecl.p, c->src.x.p, c->src.y.p, c->src.z.p, c->src.q.p, c->src4.p,
+           c->rows.p, stats);
+  k_unpermute<<<grid_for(n_t, 256), 256, 0, st>>>(n_t, c->out_sorted.p, c->tgt->perm.p, phi_dev);
+  BLTC_LAUNCH_CHECK();
+  ++c->launches;
+  tm.mark();  // 3
+  if (stats) {
+    unsigned long long* h = (unsigned long long*)c->hs.get(64);
+    BLTC_CUDA(cudaMemcpyAsync(h, c->lists.pairs.p, 2 * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, st));
+    BLTC_CUDA(cudaStreamSynchronize(st));
+    stats->n_clusters = nn;
+    stats->n_batches = c->bstart.n;
+    stats->direct_pairs = (int64_t)h[0];
+    stats->approx_pairs = (int64_t)h[1];
+    stats->setup_s = tm.secs(0, 1);
+    stats->precompute_s = tm.secs(1, 2);
+    stats->compute_s = tm.secs(2, 3);
+    stats->total_s = tm.secs(0, 3);
+    stats->n_moments = c->n_moments;
+    stats->kernel_launches = c->launches;
+    stats->tree_depth = c->src.depth;
+    stats->batch_depth = c->tgt->depth;
+  } else {
+    BLTC_CUDA(cudaStreamSynchronize(st));
+  }
+  c->have_run = true;
+}
+
+void require_run(bltc_ctx* c) {
+  if (!c || !c->have_run) {
+    set_error("no completed run on this context");
+    throw UserError{BLTC_ERR_STATE};
+  }
+}
+
+template <typename T>
+void d2h(T* host, const T* dev, int64_t n, cudaStream_t st) {
+  if (host && n > 0) BLTC_CUDA(cudaMemcpyAsync(host, dev, n * sizeof(T), cudaMemcpyDeviceToHost, st));
+}
+
+void d2h_widen(bltc_ctx* c, int64_t* host, const int32_t* dev, int64_t n) {
+  if (!host || n <= 0) return;
+  c->widen.resize(n);
+  k_widen<<<grid_for(n, 256), 256, 0, c->st>>>(n, dev, c->widen.p);
+  BLTC_LAUNCH_CHECK();
+  d2h(host, c->widen.p, n, c->st);
+  BLTC_CUDA(cudaStreamSynchronize(c->st));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bltc_last_error(void) { return g_err.c_str(); }
+const char* bltc_version(void) { return "libbltc 0.1 (sm_100a)"; }
+
+int bltc_create(int device, void* stream, bltc_ctx** out) {
+  return guarded([&] {
+    if (!out) {
+      set_error("out is NULL");
+      throw UserError{BLTC_ERR_VALUE};
+    }
+    bltc_ctx* c = new bltc_ctx();
+    if (device < 0) BLTC_CUDA(cudaGetDevice(&device));
+    c->device = device;
+    BLTC_CUDA(cudaSetDevice(device));
+    if (stream) {
+      c->st = (cudaStream_t)stream;
+    } else {
+      BLTC_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    *out = c;
+  });
+}
+
+int bltc_destroy(bltc_ctx* c) {
+  return guarded([&] {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->st);
+    Partition* ps[2] = {&c->src, &c->tgt_own};
+    for (Partition* P : ps) {
+      P->x.release(); P->y.release(); P->z.release(); P->q.release(); P->order.release();
+      P->perm.release(); P->start.release(); P->stop.release(); P->child_start.release();
+      P->child_count.release(); P->level.release(); P->lo.release(); P->hi.release();
+      P->leaves.release();
+    }
+    BuildScratch& S = c->bs;
+    S.x1.release(); S.y1.release(); S.z1.release(); S.q1.release(); S.o1.release();
+    S.node_of0.release(); S.node_of1.release(); S.code.release(); S.tile_cnt.release();
+    S.node_base.release(); S.node_off.release(); S.node_child.release(); S.node_nchild.release();
+    S.node_split.release(); S.node_mid.release(); S.box_u.release(); S.scan_tmp.release();
+    S.counter.release();
+    for (auto& b : c->in) b.release();
+    c->mac.release(); c->ecl.release(); c->bcenter.release(); c->bradius.release();
+    c->bstart.release(); c->bstop.release();
+    Lists& L = c->lists;
+    L.a_ptr.release(); L.d_ptr.release(); L.a_idx.release(); L.d_idx.release();
+    L.a_cnt.release(); L.d_cnt.release(); L.pairs.release();
+    c->used.release(); c->mflag.release(); c->mpos.release(); c->mlist.release();
+    c->rows.release(); c->s_nodes.release(); c->w_nodes.release(); c->out_sorted.release();
+    c->far_out.release(); c->phi_dev.release(); c->src4.release(); c->flag.release();
+    c->widen.release(); c->f_ecl.release(); c->f_mac.release(); c->f_x.release();
+    c->f_y.release(); c->f_z.release(); c->f_q.release(); c->f_rows.release();
+    c->f_src4.release();
+    c->hs.release();
+    if (c->own_stream) cudaStreamDestroy(c->st);
+    delete c;
+  });
+}
+
+int bltc_set_timing(bltc_ctx* c, int enable) {
+  return guarded([&] {
+    if (!c) throw UserError{BLTC_ERR_VALUE};
+    c->timing = enable != 0;
+  });
+}
+
+int bltc_treecode_device(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64_t n_t,
+                         const double* tx, const double* ty, const double* tz, int64_t n_s,
+                         const double* sx, const double* sy, const double* sz, const double* q,
+                         int32_t coincident, double* phi_out, bltc_stats* stats) {
+  return guarded([&] {
+    if (!c) throw UserError{BLTC_ERR_VALUE};
+    BLTC_CUDA(cudaSetDevice(c->device));
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    run_pipeline(c, p, cheb_s, n_t, tx, ty, tz, n_s, sx, sy, sz, q, coincident != 0, phi_out,
+                 stats);
+  });
+}
+
+int bltc_treecode(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64_t n_t,
+                  const double* tx, const double* ty, const double* tz, int64_t n_s,
+                  const double* sx, const double* sy, const double* sz, const double* q,
+                  int32_t coincident, double* phi_out, bltc_stats* stats) {
+  return guarded([&] {
+    if (!c) throw UserError{BLTC_ERR_VALUE};
+    BLTC_CUDA(cudaSetDevice(c->device));
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    check_params(p);
+    if (n_s < 1 || n_t < 1) {
+      set_error("cannot partition an empty particle set");
+      throw UserError{BLTC_ERR_VALUE};
+    }
+    cudaStream_t st = c->st;
+    cudaEvent_t e0, e1, e2, e3;
+    BLTC_CUDA(cudaEventCreate(&e0));
+    BLTC_CUDA(cudaEventCreate(&e1));
+    BLTC_CUDA(cudaEventCreate(&e2));
+    BLTC_CUDA(cudaEventCreate(&e3));
+    BLTC_CUDA(cudaEventRecord(e0, st));
+    const double* hs_[7] = {tx, ty, tz, sx, sy, sz, q};
+    const int64_t ns_[7] = {n_t, n_t, n_t, n_s, n_s, n_s, n_s};
+    for (int k = 0; k < 7; ++k) {
+      if (coincident && k < 3) continue;
+      c->in[k].resize(ns_[k]);
+      BLTC_CUDA(cudaMemcpyAsync(c->in[k].p, hs_[k], ns_[k] * sizeof(double),
+                                cudaMemcpyHostToDevice, st));
+    }
+    BLTC_CUDA(cudaEventRecord(e1, st));
+    c->phi_dev.resize(n_t);
+    const bool co = coincident != 0;
+    run_pipeline(c, p, cheb_s, n_t, co ? c->in[3].p : c->in[0].p, co ? c->in[4].p : c->in[1].p,
+                 co ? c->in[5].p : c->in[2].p, n_s, c->in[3].p, c->in[4].p, c->in[5].p,
+                 c->in[6].p, co, c->phi_dev.p, stats);
+    BLTC_CUDA(cudaEventRecord(e2, st));
+    BLTC_CUDA(cudaMemcpyAsync(phi_out, c->phi_dev.p, n_t * sizeof(double),
+                              cudaMemcpyDeviceToHost, st));
+    BLTC_CUDA(cudaEventRecord(e3, st));
+    BLTC_CUDA(cudaEventSynchronize(e3));
+    float a = 0, b = 0;
+    BLTC_CUDA(cudaEventElapsedTime(&a, e0, e1));
+    BLTC_CUDA(cudaEventElapsedTime(&b, e2, e3));
+    if (stats) {
+      stats->h2d_s = a * 1e-3;
+      stats->d2h_s = b * 1e-3;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    cudaEventDestroy(e3);
+  });
+}
+
+int bltc_get_sizes(bltc_ctx* c, bltc_sizes* out) {
+  return guarded([&] {
+    require_run(c);
+    out->n_sources = c->src.n;
+    out->n_targets = c->tgt->n;
+    out->n_clusters = c->src.n_nodes;
+    out->n_batches = c->bstart.n;
+    out->n_approx = c->lists.n_approx;
+    out->n_direct = c->lists.n_direct;
+    out->n_moments = c->n_moments;
+    out->degree = c->params.degree;
+    out->tree_depth = c->src.depth;
+    out->batch_depth = c->tgt->depth;
+  });
+}
+
+int bltc_export_tree(bltc_ctx* c, int which, int64_t* n_nodes_out, int64_t* perm, int64_t* start,
+                     int64_t* stop, double* lo, double* hi, int64_t* child_start,
+                     int64_t* child_count, int32_t* level) {
+  return guarded([&] {
+    require_run(c);
+    BLTC_CUDA(cudaSetDevice(c->device));
+    const Partition& P = which == 0 ? c->src : *c->tgt;
+    if (n_nodes_out) *n_nodes_out = P.n_nodes;
+    d2h_widen(c, perm, P.perm.p, P.n);
+    d2h_widen(c, start, P.start.p, P.n_nodes);
+    d2h_widen(c, stop, P.stop.p, P.n_nodes);
+    d2h_widen(c, child_start, P.child_start.p, P.n_nodes);
+    d2h_widen(c, child_count, P.child_count.p, P.n_nodes);
+    d2h(lo, P.lo.p, 3 * P.n_nodes, c->st);
+    d2h(hi, P.hi.p, 3 * P.n_nodes, c->st);
+    d2h(level, P.level.p, P.n_nodes, c->st);
+    BLTC_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+int bltc_export_batches(bltc_ctx* c, int64_t* start, int64_t* stop, double* center,
+                        double* radius) {
+  return guarded([&] {
+    require_run(c);
+    BLTC_CUDA(cudaSetDevice(c->device));
+    const int64_t nb = c->bstart.n;
+    d2h_widen(c, start, c->bstart.p, nb);
+    d2h_widen(c, stop, c->bstop.p, nb);
+    d2h(center, c->bcenter.p, 3 * nb, c->st);
+    d2h(radius, c->bradius.p, nb, c->st);
+    BLTC_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+int bltc_export_lists(bltc_ctx* c, int64_t* a_ptr, int64_t* a_idx, int64_t* d_ptr,
+                      int64_t* d_idx) {
+  return guarded([&] {
+    require_run(c);
+    BLTC_CUDA(cudaSetDevice(c->device));
+    const Lists& L = c->lists;
+    const int64_t nseg = L.nb * L.n_groups;
+    d2h_widen(c, a_ptr, L.a_ptr.p, nseg + 1);
+    d2h_widen(c, d_ptr, L.d_ptr.p, nseg + 1);
+    d2h_widen(c, a_idx, L.a_idx.p, L.n_approx);
+    d2h_widen(c, d_idx, L.d_idx.p, L.n_direct);
+  });
+}
+
+int bltc_export_moments(bltc_ctx* c, int64_t* cluster_ids, double* rows) {
+  return guarded([&] {
+    require_run(c);
+    BLTC_CUDA(cudaSetDevice(c->device));
+    const int m = c->params.degree + 1;
+    d2h_widen(c, cluster_ids, c->mlist.p, c->n_moments);
+    d2h(rows, c->rows.p, c->n_moments * (int64_t)m * m * m, c->st);
+    BLTC_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+int bltc_rank_build(bltc_ctx*, const bltc_params*, const double*, int64_t, const double*,
+                    const double*, const double*, const double*, int32_t) {
+  set_error("not implemented yet");
+  return BLTC_ERR_UNSUPPORTED;
+}
+int bltc_rank_publish_sizes(bltc_ctx*, bltc_publish_sizes*) {
+  set_error("not implemented yet");
+  return BLTC_ERR_UNSUPPORTED;
+}
+int bltc_rank_publish(bltc_ctx*, double*, double*, double*) {
+  set_error("not implemented yet");
+  return BLTC_ERR_UNSUPPORTED;
+}
+int bltc_rank_evaluate(bltc_ctx*, const bltc_params*, int32_t, int32_t, const int64_t*,
+                       const int64_t*, const int64_t*, const double* const*,
+                       const double* const*, const double* const*, double*, int32_t,
+                       bltc_stats*) {
+  set_error("not implemented yet");
+  return BLTC_ERR_UNSUPPORTED;
+}
+
+}  // extern "C"

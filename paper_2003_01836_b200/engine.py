@@ -1,0 +1,249 @@
+"""Drop-in BLTC evaluation entry point on B200 (engine.py of the reference).
+
+``treecode_potentials(system, config, threads=1)`` keeps the reference's
+signature and return value (engine.py:350-372): potentials in the caller's
+original target order plus a :class:`RunStats`.  Every stage -- source tree,
+target batches, interaction lists, moments, far/near-field sums,
+un-permute -- runs in libbltc's sm_100a CUDA kernels; this module only
+validates arguments (raising the reference's ``ValueError``s) and moves
+buffers across the C ABI.
+
+``system`` may be this package's :class:`~.particles.ParticleSystem` or the
+reference's own object (duck typed: ``targets``/``sources`` with float64
+``x, y, z``; ``charges``; ``targets is sources`` means coincident).
+``config`` may be this package's :class:`EvalConfig` or the reference's.
+
+Modes: ``"parity"`` reproduces the reference bit for bit (IEEE sqrt/div, no
+FMA, reference accumulation order); ``"fast"`` is the performance path
+(rsqrt + FMA, register-blocked tiles) validated against it.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .kernels import KernelSpec, coulomb
+from .particles import ParticleSystem
+
+DEFAULT_MODE = os.environ.get("BLTC_MODE", "fast")
+_MODES = {"parity": _lib.MODE_PARITY, "fast": _lib.MODE_FAST}
+
+
+@dataclass(frozen=True)
+class EvalConfig:
+    """Treecode parameters for one run (engine.py:46-62)."""
+
+    theta: float
+    degree: int
+    leaf_size: int = 2000
+    batch_size: int = 2000
+    kernel: KernelSpec = field(default_factory=coulomb)
+
+    def __post_init__(self):
+        if not (0.0 < self.theta <= 1.0):
+            raise ValueError(f"theta must be in (0, 1], got {self.theta}")
+        if self.degree < 0:
+            raise ValueError("degree must be >= 0")
+        if self.leaf_size < 1 or self.batch_size < 1:
+            raise ValueError("leaf_size and batch_size must be >= 1")
+
+
+@dataclass(eq=False)
+class RunStats:
+    """engine.py:338-347 plus device detail (times are CUDA-event seconds)."""
+
+    n_clusters: int
+    n_batches: int
+    direct_pairs: int
+    approx_pairs: int
+    setup_s: float
+    precompute_s: float
+    compute_s: float
+    total_s: float
+    h2d_s: float = 0.0
+    d2h_s: float = 0.0
+    far_s: float = 0.0
+    near_s: float = 0.0
+    n_moments: int = 0
+    kernel_launches: int = 0
+    tree_depth: int = 0
+    batch_depth: int = 0
+
+    @classmethod
+    def from_c(cls, s: _lib.Stats) -> "RunStats":
+        return cls(**{name: getattr(s, name) for name, _ in _lib.Stats._fields_})
+
+
+def cheb_nodes(degree: int) -> np.ndarray:
+    """Normalised second-kind Chebyshev nodes s_k = sin(pi (n - 2k) / (2n))
+    (interp.py:52), computed with numpy on the host so the device grids are
+    bitwise those of the reference (no device sin)."""
+    if degree == 0:
+        return np.zeros(1)
+    k = np.arange(degree + 1)
+    return np.ascontiguousarray(np.sin(np.pi * (degree - 2 * k) / (2 * degree)))
+
+
+def make_params(config, mode: str | None = None, all_moments: bool = False) -> _lib.Params:
+    mode = DEFAULT_MODE if mode is None else mode
+    if mode not in _MODES:
+        raise ValueError(f"mode must be one of {sorted(_MODES)}, got {mode!r}")
+    theta, degree = float(config.theta), int(config.degree)
+    if not (0.0 < theta <= 1.0):
+        raise ValueError(f"theta must be in (0, 1], got {theta}")
+    if degree < 0:
+        raise ValueError("degree must be >= 0")
+    if int(config.leaf_size) < 1 or int(config.batch_size) < 1:
+        raise ValueError("leaf_size and batch_size must be >= 1")
+    kernel = config.kernel
+    kappa = float(kernel.kappa)
+    if not np.isfinite(kappa) or kappa < 0.0:
+        raise ValueError(f"kappa must be finite and >= 0, got {kappa}")
+    return _lib.Params(theta=theta, degree=degree, kernel_code=int(kernel.code),
+                       leaf_size=int(config.leaf_size), batch_size=int(config.batch_size),
+                       kappa=kappa, mode=_MODES[mode], all_moments=1 if all_moments else 0)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Context:
+    """One libbltc context (device buffers + stream) on one CUDA device."""
+
+    def __init__(self, device: int = -1, stream: int | None = None):
+        self._lib = _lib.load()
+        h = ctypes.c_void_p()
+        _lib.check(self._lib.bltc_create(int(device), ctypes.c_void_p(stream or 0),
+                                         ctypes.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.check(self._lib.bltc_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_timing(self, enable: bool) -> None:
+        _lib.check(self._lib.bltc_set_timing(self.handle, 1 if enable else 0))
+
+    # -- full pipeline -------------------------------------------------------
+    def treecode(self, system, config, mode: str | None = None, all_moments: bool = False,
+                 out: np.ndarray | None = None):
+        p = make_params(config, mode, all_moments)
+        t, s = system.targets, system.sources
+        coincident = t is s
+        sx, sy, sz = _f64(s.x), _f64(s.y), _f64(s.z)
+        q = _f64(system.charges)
+        if q.shape[0] != sx.shape[0]:
+            raise ValueError("one charge per source particle required")
+        if coincident:
+            tx, ty, tz = sx, sy, sz
+        else:
+            tx, ty, tz = _f64(t.x), _f64(t.y), _f64(t.z)
+        n_t, n_s = tx.shape[0], sx.shape[0]
+        if n_s == 0 or n_t == 0:
+            raise ValueError("cannot partition an empty particle set")
+        phi = np.empty(n_t) if out is None else out
+        st = _lib.Stats()
+        nodes = cheb_nodes(p.degree)
+        _lib.check(self._lib.bltc_treecode(
+            self.handle, ctypes.byref(p), _lib.f64p(nodes), n_t, _lib.f64p(tx), _lib.f64p(ty),
+            _lib.f64p(tz), n_s, _lib.f64p(sx), _lib.f64p(sy), _lib.f64p(sz), _lib.f64p(q),
+            1 if coincident else 0, _lib.f64p(phi), ctypes.byref(st)))
+        return phi, RunStats.from_c(st)
+
+    def treecode_device(self, params: _lib.Params, n_t, tx, ty, tz, n_s, sx, sy, sz, q,
+                        coincident: bool, phi_ptr) -> RunStats:
+        """Device-pointer variant (inputs resident in HBM): raw integer pointers."""
+        st = _lib.Stats()
+        nodes = cheb_nodes(params.degree)
+        _lib.check(self._lib.bltc_treecode_device(
+            self.handle, ctypes.byref(params), _lib.f64p(nodes), int(n_t), tx, ty, tz, int(n_s),
+            sx, sy, sz, q, 1 if coincident else 0, phi_ptr, ctypes.byref(st)))
+        return RunStats.from_c(st)
+
+    # -- stage exports of the last run (bit-exact structure checks) ------------
+    def sizes(self) -> _lib.Sizes:
+        sz = _lib.Sizes()
+        _lib.check(self._lib.bltc_get_sizes(self.handle, ctypes.byref(sz)))
+        return sz
+
+    def export_tree(self, which: int = 0) -> dict:
+        sz = self.sizes()
+        n = sz.n_sources if which == 0 else sz.n_targets
+        nn = ctypes.c_int64()
+        _lib.check(self._lib.bltc_export_tree(self.handle, which, ctypes.byref(nn), None, None,
+                                              None, None, None, None, None, None))
+        nn = nn.value
+        out = dict(perm=np.empty(n, np.int64), start=np.empty(nn, np.int64),
+                   stop=np.empty(nn, np.int64), lo=np.empty((nn, 3)), hi=np.empty((nn, 3)),
+                   child_start=np.empty(nn, np.int64), child_count=np.empty(nn, np.int64),
+                   level=np.empty(nn, np.int32))
+        _lib.check(self._lib.bltc_export_tree(
+            self.handle, which, None, _lib.i64p(out["perm"]), _lib.i64p(out["start"]),
+            _lib.i64p(out["stop"]), _lib.f64p(out["lo"]), _lib.f64p(out["hi"]),
+            _lib.i64p(out["child_start"]), _lib.i64p(out["child_count"]),
+            _lib.i32p(out["level"])))
+        return out
+
+    def export_batches(self) -> dict:
+        nb = self.sizes().n_batches
+        out = dict(start=np.empty(nb, np.int64), stop=np.empty(nb, np.int64),
+                   center=np.empty((nb, 3)), radius=np.empty(nb))
+        _lib.check(self._lib.bltc_export_batches(self.handle, _lib.i64p(out["start"]),
+                                                 _lib.i64p(out["stop"]),
+                                                 _lib.f64p(out["center"]),
+                                                 _lib.f64p(out["radius"])))
+        return out
+
+    def export_lists(self) -> dict:
+        sz = self.sizes()
+        out = dict(a_ptr=np.empty(sz.n_batches + 1, np.int64), a_idx=np.empty(sz.n_approx, np.int64),
+                   d_ptr=np.empty(sz.n_batches + 1, np.int64), d_idx=np.empty(sz.n_direct, np.int64))
+        _lib.check(self._lib.bltc_export_lists(self.handle, _lib.i64p(out["a_ptr"]),
+                                               _lib.i64p(out["a_idx"]), _lib.i64p(out["d_ptr"]),
+                                               _lib.i64p(out["d_idx"])))
+        return out
+
+    def export_moments(self):
+        sz = self.sizes()
+        m3 = (sz.degree + 1) ** 3
+        ids = np.empty(sz.n_moments, np.int64)
+        rows = np.empty((sz.n_moments, m3))
+        _lib.check(self._lib.bltc_export_moments(self.handle, _lib.i64p(ids), _lib.f64p(rows)))
+        return ids, rows
+
+
+_default_ctx: dict[int, Context] = {}
+
+
+def default_context(device: int = -1) -> Context:
+    ctx = _default_ctx.get(device)
+    if ctx is None:
+        ctx = Context(device)
+        _default_ctx[device] = ctx
+    return ctx
+
+
+def treecode_potentials(system: ParticleSystem, config: EvalConfig, threads: int = 1,
+                        mode: str | None = None, context: Context | None = None
+                        ) -> tuple[np.ndarray, RunStats]:
+    """Full pipeline on the GPU (engine.py:350-372).
+
+    ``threads`` is accepted for signature compatibility and ignored: the
+    device schedules target batches itself (the reference's results are
+    thread-count invariant, test_engine.py:241-248, and so are these).
+    """
+    del threads
+    ctx = context or default_context()
+    return ctx.treecode(system, config, mode=mode)
