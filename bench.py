@@ -1,0 +1,409 @@
+#!/usr/bin/env python
+"""BLTC evaluation benchmark (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4]
+                    [--impl ours|reference] [--mode fast|parity]
+
+One step = one full BLTC evaluation of the workload (source tree, target
+batches, interaction lists, moments, far + near field, un-permute) through
+libbltc's CUDA kernels, inputs resident in HBM.  ``value`` is particles/s
+over all ranks; ``e2e`` is the same metric through the public API with
+host (pinned) buffers, H2D/D2H inside the timed region.  ``roofline`` is the
+dominant kernel's (far field) FP64 throughput against the device's FP64 FMA
+peak measured live in the same process.  ``cpu_baseline`` is the CPU
+restatement of the reference algorithm (oracle/, "port") on the host cores
+on a bounded sample.
+
+N > 1 (torchrun, one rank per GPU): targets are partitioned by recursive
+coordinate bisection (decomp.py:76-130), each rank builds its tree and
+moments, one all-gather over NCCL replicates the forest, each rank
+evaluates its batches; timing is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BLTC eval time & particles/s (N=8M Coulomb n=8 θ=0.8), %FP64 peak, 1/2/4/8 GPU"
+
+CONFIGS = {
+    # BASELINE.json configs; c4 is the metric's workload (8M Coulomb n=8 theta=0.8)
+    "c1": dict(workload="C1: N=20k uniform cube, Coulomb, n=4, theta=0.7", gen="uniform",
+               n=20_000, kind=0, kappa=0.0, degree=4, theta=0.7, leaf=2000, batch=2000),
+    "c2": dict(workload="C2: N=1M uniform cube, Coulomb, n=8, theta=0.8", gen="uniform",
+               n=1_000_000, kind=0, kappa=0.0, degree=8, theta=0.8, leaf=2000, batch=2000),
+    "c3": dict(workload="C3: N=1M uniform cube, Yukawa kappa=0.5, n=8, theta=0.8",
+               gen="uniform", n=1_000_000, kind=1, kappa=0.5, degree=8, theta=0.8, leaf=2000,
+               batch=2000),
+    "c4": dict(workload="C4: N=8M Plummer (a=1, r<=10a), Coulomb, n=8, theta=0.8",
+               gen="plummer", n=8_000_000, kind=0, kappa=0.0, degree=8, theta=0.8, leaf=2000,
+               batch=2000),
+    "c4u": dict(workload="N=8M uniform cube, Coulomb, n=8, theta=0.8", gen="uniform",
+                n=8_000_000, kind=0, kappa=0.0, degree=8, theta=0.8, leaf=2000, batch=2000),
+    "c5": dict(workload="C5: N=64M uniform cube, Coulomb, n=10, theta=0.7", gen="uniform",
+               n=64_000_000, kind=0, kappa=0.0, degree=10, theta=0.7, leaf=2000, batch=2000),
+}
+
+# Minimal FP64-pipe slots per pair: far / near field.
+SLOTS = {0: (7, 12), 1: (25, 30), 2: (1, 1)}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+              "power.draw")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out, _ = self.proc.communicate()
+
+    def summary(self) -> dict:
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[3:7],
+                             float(parts[7]) if parts[7] not in ("", "[N/A]") else 0.0))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k, v in enumerate(r[2]) if v == "Active"})
+        return {"sm_mhz": float(np.median([r[0] for r in rows])),
+                "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "power_w_max": max(r[3] for r in rows), "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+
+
+def make_system(cfg: dict, seed: int = 1):
+    from paper_2003_01836_b200 import cli
+    gen = cli.generate_particles if cfg["gen"] == "uniform" else cli.generate_plummer
+    return gen(cfg["n"], seed)
+
+
+def eval_config(cfg: dict, batch: int | None, leaf: int | None):
+    from paper_2003_01836_b200 import EvalConfig, coulomb, test_constant, yukawa
+    kernel = [coulomb(), yukawa(cfg["kappa"]), test_constant()][cfg["kind"]]
+    return EvalConfig(theta=cfg["theta"], degree=cfg["degree"],
+                      leaf_size=leaf or cfg["leaf"], batch_size=batch or cfg["batch"],
+                      kernel=kernel)
+
+
+def probe_fp64(device: int) -> float:
+    import ctypes
+    from paper_2003_01836_b200 import _lib
+    lib = _lib.load()
+    v = ctypes.c_double()
+    _lib.check(lib.bltc_probe_fp64(device, 0.3, ctypes.byref(v)))
+    return v.value
+
+
+def cpu_baseline(system, cfg, econf, budget_pairs: float = 1.5e10, threads: int | None = None):
+    """Oracle (C restatement of the reference path) on the host cores,
+    bounded: full tree / batches / lists / moments, evaluation on a random
+    sample of target batches, extrapolated by pair count."""
+    from oracle import oracle as orc
+    threads = threads or os.cpu_count() or 1
+    s = system.sources
+    t0 = time.perf_counter()
+    tree = orc.build_source_tree(s.x, s.y, s.z, system.charges, econf.leaf_size)
+    if econf.batch_size == econf.leaf_size:
+        lf = tree.leaf_dfs
+        batches = orc.Batches(tree=tree, start=tree.start[lf], stop=tree.stop[lf],
+                              center=tree.center[lf], radius=tree.radius[lf])
+    else:
+        batches = orc.build_target_batches(s.x, s.y, s.z, econf.batch_size)
+    lists = orc.build_lists(batches, tree, econf.theta, econf.degree)
+    t1 = time.perf_counter()
+    rows, mrow = orc.compute_moments(tree, econf.degree, np.unique(lists.a_idx), threads)
+    t2 = time.perf_counter()
+    nt = batches.stop - batches.start
+    m3 = (econf.degree + 1) ** 3
+    csum = np.concatenate([[0], np.cumsum(tree.count[lists.d_idx])])
+    dpairs = nt * (csum[lists.d_ptr[1:]] - csum[lists.d_ptr[:-1]])
+    apairs = nt * m3 * np.diff(lists.a_ptr)
+    cost = dpairs + apairs
+    rng = np.random.default_rng(0)
+    order = rng.permutation(batches.nb)
+    take = np.searchsorted(np.cumsum(cost[order]), budget_pairs) + 1
+    sel = np.sort(order[:min(take, batches.nb)])
+    frac = float(cost[sel].sum() / cost.sum())
+    t3 = time.perf_counter()
+    orc.evaluate(batches, [orc.SourceGroup(tree, rows, mrow, lists)], econf.degree,
+                 econf.kernel.code, econf.kernel.kappa, threads, sel=sel)
+    t4 = time.perf_counter()
+    est = (t1 - t0) + (t2 - t1) + (t4 - t3) / frac
+    return {"value": system.n_targets / est, "unit": "particles/s", "cores": threads,
+            "kind": "port",
+            "sample": (f"oracle/ C port of the reference path, {threads} threads: full tree+"
+                       f"batches+lists ({t1 - t0:.1f}s, serial) and moments ({t2 - t1:.1f}s), "
+                       f"evaluation of {len(sel)}/{batches.nb} random batches = {frac:.4f} of "
+                       f"the pairs in {t4 - t3:.1f}s, extrapolated: est {est:.1f}s per step"),
+            "est_step_s": est, "setup_s": t1 - t0, "moments_s": t2 - t1,
+            "eval_sample_s": t4 - t3, "sample_frac": frac}
+
+
+# ---------------------------------------------------------------------------
+
+
+def run_reference(args, cfg):
+    """--impl reference: the reference's CPU algorithm (oracle port; the
+    Python/numba reference itself is not installable on the box) on this
+    host's cores, each step a bounded sample of the same workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    econf = eval_config(cfg, args.batch_size, args.leaf_size)
+    system = make_system(cfg)
+    vals = []
+    res = None
+    for i in range(args.warmup + args.steps):
+        res = cpu_baseline(system, cfg, econf, budget_pairs=args.ref_budget)
+        if i >= args.warmup:
+            vals.append(res["value"])
+        log(f"reference step {i}: {res['sample']}")
+    value = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "particles/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * cfg["n"] / value, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "n": cfg["n"], "theta": cfg["theta"],
+                   "degree": cfg["degree"], "leaf_size": econf.leaf_size,
+                   "batch_size": econf.batch_size, "kernel": ["coulomb", "yukawa", "const"][cfg["kind"]]},
+        "cpu_baseline": {"value": value, "unit": "particles/s", "cores": res["cores"],
+                         "kind": res["kind"], "sample": res["sample"]},
+        "e2e": {"value": value, "unit": "particles/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg):
+    import torch
+
+    import paper_2003_01836_b200 as bltc
+    from paper_2003_01836_b200 import engine
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    econf = eval_config(cfg, args.batch_size, args.leaf_size)
+    system = make_system(cfg)
+    n = cfg["n"]
+    stream = torch.cuda.current_stream()
+    ctx = bltc.Context(local, stream.cuda_stream)
+    mode = args.mode
+    params = engine.make_params(econf, mode)
+    dfma = probe_fp64(local)
+    peak_tflops = 2.0 * dfma / 1e12
+
+    if world > 1:
+        from paper_2003_01836_b200 import decomp
+        runner = decomp.DeviceRankRunner(ctx, system, econf, mode=mode, group=dist.group.WORLD)
+        step = runner.step
+        n_local = runner.n_local
+    else:
+        s = system.sources
+        dev = [torch.from_numpy(a).cuda() for a in (s.x, s.y, s.z, system.charges)]
+        phi = torch.empty(n, dtype=torch.float64, device="cuda")
+        ptrs = [t.data_ptr() for t in dev]
+
+        def step():
+            return ctx.treecode_device(params, n, ptrs[0], ptrs[1], ptrs[2], n, ptrs[0],
+                                       ptrs[1], ptrs[2], ptrs[3], True, phi.data_ptr())
+        n_local = n
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    stats = []
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            stats.append(step())
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = n / (ms * 1e-3)
+
+    st = stats[-1]
+    far_s = float(np.mean([x.far_s for x in stats]))
+    near_s = float(np.mean([x.near_s for x in stats]))
+    s_far, s_near = SLOTS[cfg["kind"]]
+    far_tflops = 2.0 * s_far * st.approx_pairs / far_s / 1e12 if far_s > 0 else 0.0
+    near_tflops = 2.0 * s_near * st.direct_pairs / near_s / 1e12 if near_s > 0 else 0.0
+    launches = int(sum(x.kernel_launches for x in stats))
+
+    # ---- e2e through the public API with pinned host buffers (H2D/D2H inside)
+    e2e = None
+    if world == 1:
+        s = system.sources
+        pinned = [torch.from_numpy(a).pin_memory() for a in (s.x, s.y, s.z, system.charges)]
+        hx, hy, hz, hq = [t.numpy() for t in pinned]
+        pts = bltc.Points(hx, hy, hz)
+        psys = bltc.ParticleSystem.from_single_set(pts, hq)
+        out = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
+        for _ in range(2):
+            bltc.treecode_potentials(psys, econf, mode=mode, context=ctx)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            ctx.treecode(psys, econf, mode=mode, out=out)
+        t1 = time.perf_counter()
+        e2e_s = (t1 - t0) / args.steps
+        e2e = {"value": n / e2e_s, "unit": "particles/s", "h2d_bytes_per_step": 4 * 8 * n,
+               "d2h_bytes_per_step": 8 * n, "ms_per_step": 1e3 * e2e_s,
+               "api": "paper_2003_01836_b200.Context.treecode (treecode_potentials) -> bltc_treecode"}
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "far_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                tj = json.load(f)
+            if tj.get("config") == args.config and tj.get("batch_size") == econf.batch_size:
+                traffic = tj.get("bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "n": n, "theta": cfg["theta"],
+                   "degree": cfg["degree"], "leaf_size": econf.leaf_size,
+                   "batch_size": econf.batch_size,
+                   "kernel": ["coulomb", "yukawa", "const"][cfg["kind"]], "mode": mode,
+                   "parallelism": f"rcb{world}" if world > 1 else "single",
+                   "l2": "inputs (32 B/particle = 256 MB at 8M) larger than the 126 MB L2"},
+        "phases_s": {"setup": st.setup_s, "precompute": st.precompute_s,
+                     "compute": st.compute_s, "far": far_s, "near": near_s},
+        "pairs": {"approx": st.approx_pairs, "direct": st.direct_pairs,
+                  "clusters": st.n_clusters, "batches": st.n_batches,
+                  "moments": st.n_moments},
+        "roofline": {"bound": "fp64", "kernel": "k_far_fast (far field)",
+                     "achieved": far_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
+                     "frac": far_tflops / peak_tflops if peak_tflops else None,
+                     "traffic": traffic,
+                     "work": f"{s_far} FP64 slots/pair x approx pairs (2 flop/slot)",
+                     "peak_source": "DFMA microbenchmark on this GPU in this run (bltc_probe_fp64)"},
+        "near_roofline": {"kernel": "k_near_fast (near field)", "achieved": near_tflops,
+                          "frac": near_tflops / peak_tflops if peak_tflops else None,
+                          "work": f"{s_near} FP64 slots/pair x direct pairs"},
+        "interaction_frac": ((2.0 * (s_far * st.approx_pairs + s_near * st.direct_pairs)
+                              / (far_s + near_s) / 1e12) / peak_tflops
+                             if far_s + near_s > 0 else None),
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cb = cpu_baseline(system, cfg, econf, budget_pairs=args.ref_budget)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind",
+                                                      "sample")}
+        except Exception as exc:   # the baseline is reported, never required
+            line["cpu_baseline"] = {"value": None, "error": repr(exc)}
+    print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c4")
+    ap.add_argument("--mode", choices=["fast", "parity"], default="fast")
+    ap.add_argument("--batch-size", type=int, default=None)
+    ap.add_argument("--leaf-size", type=int, default=None)
+    ap.add_argument("--ref-budget", type=float, default=1.5e10,
+                    help="pairs evaluated by the CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("note: --warmup raised to 3 (timing rules)")
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -169,6 +169,11 @@ BLTC_API int bltc_rank_evaluate(bltc_ctx* ctx, const bltc_params* p, int32_t ran
                        const double* const* particles, const double* const* moments,
                        double* phi_out, int32_t device_ptrs, bltc_stats* stats);
 
+/* ---- Diagnostics --------------------------------------------------------
+ * Sustained FP64 FMA throughput of the device (DFMA/s), measured for about
+ * `seconds`: the denominator of the FP64 roofline fraction bench.py reports. */
+BLTC_API int bltc_probe_fp64(int device, double seconds, double* dfma_per_s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -85,6 +85,7 @@ SIGNATURES = {
                                           ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                                           ctypes.POINTER(_vp), _vp, ctypes.c_int32,
                                           ctypes.POINTER(Stats)]),
+    "bltc_probe_fp64": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _f64p]),
 }
 
 _lib = None

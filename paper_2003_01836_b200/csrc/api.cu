@@ -2,7 +2,10 @@
 // replaces treecode_potentials (engine.py:350-372), stage exports for the
 // bit-exact checks, and the per-rank entry points of the distributed path
 // (decomp.py:483-593).
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -13,13 +16,14 @@
 namespace bltc {
 
 static thread_local std::string g_err;
+long long g_launch_count = 0;
 void set_error(const std::string& msg) { g_err = msg; }
 
 __global__ void k_moments(const double* sx, const double* sy, const double* sz,
                           const double* sq, const int32_t* list, const int32_t* cstart,
                           const int32_t* cstop, const double* lo, const double* hi,
                           const double* s_nodes, const double* w_nodes, int degree,
-                          double* rows);
+                          int mstride, double* rows);
 __global__ void k_lists(int64_t nb, int G, int g, const double* bcenter, const double* bradius,
                         const int32_t* bstart, const int32_t* bstop, const MacNode* nodes,
                         int32_t cluster_offset, double theta, int64_t per_node, bool fill,
@@ -162,6 +166,9 @@ struct bltc_ctx {
   DBuf<double> s_nodes, w_nodes;
   DBuf<double> out_sorted, far_out, phi_dev;
   DBuf<double4> src4;
+  DBuf<int32_t> item_cnt, item_off, counters;
+  DBuf<int2> items;
+  DBuf<double> partial;
   DBuf<int32_t> flag;
   DBuf<int64_t> widen;
   bltc_params params{};
@@ -304,7 +311,6 @@ void build_lists(bltc_ctx* c, const bltc_params* p, int G, const MacNode* const*
                                              per_node, false, L.a_cnt.p, L.d_cnt.p, nullptr,
                                              nullptr, nullptr, nullptr, L.pairs.p, c->flag.p);
     BLTC_LAUNCH_CHECK();
-    ++c->launches;
   }
   exclusive_scan_i32(L.a_cnt.p, L.a_ptr.p, nseg + 1, c->bs.scan_tmp, st);
   exclusive_scan_i32(L.d_cnt.p, L.d_ptr.p, nseg + 1, c->bs.scan_tmp, st);
@@ -327,7 +333,6 @@ void build_lists(bltc_ctx* c, const bltc_params* p, int G, const MacNode* const*
                                              per_node, true, nullptr, nullptr, L.a_ptr.p,
                                              L.d_ptr.p, L.a_idx.p, L.d_idx.p, nullptr, c->flag.p);
     BLTC_LAUNCH_CHECK();
-    ++c->launches;
   }
 }
 
@@ -350,7 +355,6 @@ void compute_moments(bltc_ctx* c, const bltc_params* p, const Partition& T, cons
       k_mark_used<<<grid_for(c->lists.n_approx, 256), 256, 0, st>>>(
           c->lists.n_approx, c->lists.a_idx.p, c->used.p);
       BLTC_LAUNCH_CHECK();
-      ++c->launches;
     }
   }
   (void)cluster_base;
@@ -363,19 +367,25 @@ void compute_moments(bltc_ctx* c, const bltc_params* p, const Partition& T, cons
   BLTC_CUDA(cudaStreamSynchronize(st));
   c->n_moments = h[0];
   c->mlist.resize(c->n_moments + 1);
-  rows.resize(c->n_moments * m3 + 1);
+  const int mstride = moment_stride(p->degree);
+  rows.resize(c->n_moments * mstride + 2);
   k_compact_moments<<<grid_for(nn, 256), 256, 0, st>>>(nn, c->mflag.p, c->mpos.p, c->mlist.p,
                                                        ecl);
   BLTC_LAUNCH_CHECK();
-  c->launches += 3;
   if (c->n_moments > 0) {
-    int threads = ((m * m + 31) / 32) * 32;
-    if (threads < 96) threads = 96;
-    k_moments<<<(unsigned)c->n_moments, threads, 0, st>>>(
-        T.x.p, T.y.p, T.z.p, T.q.p, c->mlist.p, T.start.p, T.stop.p, T.lo.p, T.hi.p,
-        c->s_nodes.p, c->w_nodes.p, p->degree, rows.p);
-    BLTC_LAUNCH_CHECK();
-    ++c->launches;
+    if (p->mode == BLTC_MODE_FAST) {
+      launch_moments_split(T.x.p, T.y.p, T.z.p, T.q.p, c->mlist.p, c->n_moments, T.start.p,
+                           T.stop.p, T.lo.p, T.hi.p, c->s_nodes.p, c->w_nodes.p, p->degree,
+                           mstride, rows.p, c->item_cnt, c->item_off, c->items, c->partial,
+                           c->bs.scan_tmp, c->hs, st);
+    } else {
+      int threads = ((m * m + 31) / 32) * 32;
+      if (threads < 96) threads = 96;
+      k_moments<<<(unsigned)c->n_moments, threads, 0, st>>>(
+          T.x.p, T.y.p, T.z.p, T.q.p, c->mlist.p, T.start.p, T.stop.p, T.lo.p, T.hi.p,
+          c->s_nodes.p, c->w_nodes.p, p->degree, mstride, rows.p);
+      BLTC_LAUNCH_CHECK();
+    }
   }
 }
 
@@ -391,7 +401,6 @@ void build_batches(bltc_ctx* c, Partition& T) {
                                                T.stop.p, c->bstart.p, c->bstop.p, c->bcenter.p,
                                                c->bradius.p);
   BLTC_LAUNCH_CHECK();
-  c->launches += 4;
 }
 
 void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, const double* sx,
@@ -418,27 +427,48 @@ void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, 
   a.sq = sq;
   a.src4 = src4;
   a.moments = rows;
+  a.mstride = moment_stride(p->degree);
   a.s_nodes = c->s_nodes.p;
   a.degree = p->degree;
   a.kappa = p->kappa;
   c->out_sorted.resize(T.n);
   a.out = c->out_sorted.p;
-  a.work = nullptr;
   if (p->mode == BLTC_MODE_PARITY) {
     launch_eval_parity(a, p->kernel_code, st);
-    c->launches += 1;
   } else {
     c->far_out.resize(T.n);
     a.far_out = c->far_out.p;
     float far_ms = 0, near_ms = 0;
-    launch_eval_fast(a, p->kernel_code, st, st, nullptr, &far_ms, &near_ms, c->timing);
-    c->launches += 2;
+    int n_items = 0;
+    build_fast_items(a, c->item_cnt, c->item_off, c->items, c->bs.scan_tmp, c->hs, st,
+                     &n_items);
+    c->counters.resize(2);
+    launch_eval_fast(a, p->kernel_code, c->items.p, n_items, c->counters.p, st, &far_ms,
+                     &near_ms, c->timing);
     if (stats) {
       stats->far_s = far_ms * 1e-3;
       stats->near_s = near_ms * 1e-3;
     }
   }
 }
+
+// BLTC_TRACE=1: synchronise and print host wall time per pipeline stage.
+struct Trace {
+  bool on;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t;
+  explicit Trace(cudaStream_t s) : on(std::getenv("BLTC_TRACE") != nullptr), st(s) {
+    t = std::chrono::steady_clock::now();
+  }
+  void operator()(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[bltc] %-14s %9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 void run_pipeline(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64_t n_t,
                   const double* tx, const double* ty, const double* tz, int64_t n_s,
@@ -456,12 +486,14 @@ void run_pipeline(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64
   cudaStream_t st = c->st;
   c->params = *p;
   c->have_run = false;
-  c->launches = 0;
+  const long long launches0 = g_launch_count;
   Timer tm(c->timing, st);
   upload_nodes(c, p, cheb_s);
   tm.mark();  // 0
+  Trace tr(st);
   // ---- setup: source tree, target batches, interaction lists
   build_partition(c->src, c->bs, n_s, sx, sy, sz, q, p->leaf_size, st, c->hs);
+  tr("source tree");
   const bool share = coincident && p->batch_size == p->leaf_size;
   if (share) {
     c->tgt = &c->src;   // identical inputs + limits => identical partition (tree.py:225-236)
@@ -470,22 +502,27 @@ void run_pipeline(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64
                     coincident ? sz : tz, nullptr, p->batch_size, st, c->hs);
     c->tgt = &c->tgt_own;
   }
+  tr("target tree");
   build_batches(c, *c->tgt);
+  tr("batches");
   const int64_t nn = c->src.n_nodes;
   c->mac.resize(nn);
   c->ecl.resize(nn);
   k_mac_nodes<<<grid_for(nn, 128), 128, 0, st>>>(nn, c->src.lo.p, c->src.hi.p, c->src.start.p,
                                                  c->src.stop.p, c->src.child_start.p,
                                                  c->src.child_count.p, c->mac.p);
+  BLTC_LAUNCH_CHECK();
   k_eval_clusters<<<grid_for(nn, 128), 128, 0, st>>>(nn, c->src.lo.p, c->src.hi.p,
                                                      c->src.start.p, c->src.stop.p, 0, c->ecl.p);
   BLTC_LAUNCH_CHECK();
   const MacNode* trees[1] = {c->mac.p};
   const int32_t offs[1] = {0};
   build_lists(c, p, 1, trees, offs);
+  tr("lists");
   tm.mark();  // 1
   // ---- precompute: moments
   compute_moments(c, p, c->src, c->mac.p, c->ecl.p, p->all_moments ? 1 : 0, c->rows, 0);
+  tr("moments");
   tm.mark();  // 2
   // ---- compute: evaluation + un-permute
   if (p->mode == BLTC_MODE_FAST) {
@@ -493,13 +530,12 @@ void run_pipeline(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64
     k_pack4<<<grid_for(n_s, 256), 256, 0, st>>>(n_s, c->src.x.p, c->src.y.p, c->src.z.p,
                                                 c->src.q.p, c->src4.p);
     BLTC_LAUNCH_CHECK();
-    ++c->launches;
   }
   evaluate(c, p, 1, c->ecl.p, c->src.x.p, c->src.y.p, c->src.z.p, c->src.q.p, c->src4.p,
            c->rows.p, stats);
   k_unpermute<<<grid_for(n_t, 256), 256, 0, st>>>(n_t, c->out_sorted.p, c->tgt->perm.p, phi_dev);
   BLTC_LAUNCH_CHECK();
-  ++c->launches;
+  tr("evaluate");
   tm.mark();  // 3
   if (stats) {
     unsigned long long* h = (unsigned long long*)c->hs.get(64);
@@ -515,7 +551,7 @@ void run_pipeline(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64
     stats->compute_s = tm.secs(2, 3);
     stats->total_s = tm.secs(0, 3);
     stats->n_moments = c->n_moments;
-    stats->kernel_launches = c->launches;
+    stats->kernel_launches = g_launch_count - launches0;
     stats->tree_depth = c->src.depth;
     stats->batch_depth = c->tgt->depth;
   } else {
@@ -599,7 +635,8 @@ int bltc_destroy(bltc_ctx* c) {
     c->used.release(); c->mflag.release(); c->mpos.release(); c->mlist.release();
     c->rows.release(); c->s_nodes.release(); c->w_nodes.release(); c->out_sorted.release();
     c->far_out.release(); c->phi_dev.release(); c->src4.release(); c->flag.release();
-    c->widen.release(); c->f_ecl.release(); c->f_mac.release(); c->f_x.release();
+    c->widen.release(); c->item_cnt.release(); c->item_off.release(); c->counters.release();
+    c->items.release(); c->partial.release(); c->f_ecl.release(); c->f_mac.release(); c->f_x.release();
     c->f_y.release(); c->f_z.release(); c->f_q.release(); c->f_rows.release();
     c->f_src4.release();
     c->hs.release();
@@ -750,8 +787,13 @@ int bltc_export_moments(bltc_ctx* c, int64_t* cluster_ids, double* rows) {
     require_run(c);
     BLTC_CUDA(cudaSetDevice(c->device));
     const int m = c->params.degree + 1;
+    const size_t m3 = (size_t)m * m * m;
     d2h_widen(c, cluster_ids, c->mlist.p, c->n_moments);
-    d2h(rows, c->rows.p, c->n_moments * (int64_t)m * m * m, c->st);
+    if (rows && c->n_moments > 0)
+      BLTC_CUDA(cudaMemcpy2DAsync(rows, m3 * sizeof(double), c->rows.p,
+                                  moment_stride(c->params.degree) * sizeof(double),
+                                  m3 * sizeof(double), c->n_moments, cudaMemcpyDeviceToHost,
+                                  c->st));
     BLTC_CUDA(cudaStreamSynchronize(c->st));
   });
 }

@@ -55,7 +55,14 @@ void set_error(const std::string& msg);
     }                                                                          \
   } while (0)
 
-#define BLTC_LAUNCH_CHECK() BLTC_CUDA(cudaGetLastError())
+// Every kernel launch is followed by exactly one BLTC_LAUNCH_CHECK(): it
+// checks the launch and counts it (bltc_stats.kernel_launches).
+extern long long g_launch_count;
+#define BLTC_LAUNCH_CHECK()              \
+  do {                                   \
+    BLTC_CUDA(cudaGetLastError());       \
+    ++::bltc::g_launch_count;            \
+  } while (0)
 
 struct CudaFailure {};
 struct UserError {

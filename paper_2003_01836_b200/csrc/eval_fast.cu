@@ -1,31 +1,33 @@
 // FAST-mode evaluation: the two FP64-bound interaction kernels.
 //
-// far field  (_approx_tile, engine.py:216-252): batch x proxy grid
-// near field (_direct_tile, engine.py:151-213): batch x cluster particles
+//   far field  (_approx_tile, engine.py:216-252): targets x (n+1)^3 proxies
+//   near field (_direct_tile, engine.py:151-213): targets x cluster particles
 //
-// Both: one CTA per target batch (taken in descending-cost order when a work
-// list is given), 128 threads, kTpt targets per thread held in registers so
-// every shared-memory broadcast of a proxy / source feeds kTpt pairs.
-// Reciprocal square roots use the MUFU.RSQ64H seed plus one cubic correction
-// (5 FP64 ops, full double accuracy), products are fused (FMA).  Far field:
-// dz^2 is hoisted per (target, k3) and dx^2 + dy^2 per (target, k1, k2), so
-// the steady state is 1 DADD + rsqrt + 1 DFMA = 7 FP64 slots per pair.
-// Near field: 12 slots per pair; the singular-pair test (d^2 < 1e-28,
-// engine.py:175) is done on the integer pipe; per-tile partial sums are
-// folded into a Neumaier-compensated per-target total (as the reference
-// compensates per pair), keeping the result order-robust.
+// Work decomposition: a work item is (target batch, chunk of 32*kTpt
+// consecutive targets).  Persistent warps pull items from a global counter,
+// so batches of any size keep every lane busy and long interaction lists
+// balance dynamically.  Each lane holds kTpt targets in registers; every
+// proxy / source value is read once per warp from the warp's own shared-
+// memory stage (filled with cp.async) and feeds kTpt pairs.
+//
+// Arithmetic: reciprocal square roots use the MUFU.RSQ64H seed plus one
+// cubic correction (5 FP64 ops, full double accuracy); products are fused.
+//   far:  dz^2 hoisted per (target, k3), dx^2 + dy^2 per (target, k1, k2):
+//         steady state 1 DADD + rsqrt + 1 DFMA = 7 FP64 slots / pair
+//   near: 3 DADD + 1 DMUL + 2 DFMA + rsqrt + 1 DFMA = 12 slots / pair; the
+//         singular-pair test (d^2 < 1e-28, engine.py:175) runs on the integer
+//         pipe; per-chunk partial sums are folded into a Neumaier-compensated
+//         per-target total (the reference compensates per pair).
 #include "bltc_internal.cuh"
 #include "eval_common.cuh"
 
 namespace bltc {
 
 namespace {
-constexpr int kThreads = 128;
-constexpr int kTpt = 4;
-constexpr int kPass = kThreads * kTpt;
-constexpr int kSrcTile = 256;
-// bit pattern of 1e-28: for d2 >= 0, (bits(d2) >= kThrBits) <=> d2 >= 1e-28
-__device__ __forceinline__ long long thr_bits() { return __double_as_longlong(kSingularSq); }
+constexpr int kTpt = 2;                 // targets per lane
+constexpr int kChunkT = 32 * kTpt;      // targets per work item
+constexpr int kWarps = 8;               // warps per CTA
+constexpr int kSrcChunk = 64;           // near-field sources per stage
 
 __device__ __forceinline__ double rsqrt_fast(double x) {
   double y;
@@ -37,17 +39,6 @@ __device__ __forceinline__ double rsqrt_fast(double x) {
   return fma(ye, c, y);
 }
 
-template <int KIND>
-__device__ __forceinline__ double far_accum(double acc, double q, double d2, double kappa) {
-  if (KIND == 0) return fma(q, rsqrt_fast(d2), acc);
-  if (KIND == 1) {
-    const double y = rsqrt_fast(d2);
-    const double r = __dmul_rn(d2, y);
-    return fma(__dmul_rn(q, exp(-kappa * r)), y, acc);
-  }
-  return __dadd_rn(acc, q);
-}
-
 __device__ __forceinline__ void neumaier(double& acc, double& comp, double t) {
   const double s = __dadd_rn(acc, t);
   const bool big = fabs(acc) >= fabs(t);
@@ -56,39 +47,68 @@ __device__ __forceinline__ void neumaier(double& acc, double& comp, double t) {
   acc = s;
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ int next_item(int* counter) {
+  int it = 0;
+  if ((threadIdx.x & 31) == 0) it = atomicAdd(counter, 1);
+  return __shfl_sync(0xffffffffu, it, 0);
+}
+
+template <int KIND>
+__device__ __forceinline__ double far_term(double acc, double qv, double d2, double kappa) {
+  if (KIND == 0) return fma(qv, rsqrt_fast(d2), acc);
+  const double y = rsqrt_fast(d2);
+  const double r = __dmul_rn(d2, y);
+  return fma(__dmul_rn(qv, exp(-kappa * r)), y, acc);
+}
+
 // ---------------------------------------------------------------------------
-// Far field.  M = n + 1 known at compile time (unrolled k3); M = 0 is the
-// generic runtime-degree variant.
+// Far field.  M = n + 1 at compile time (k3 unrolled); M = 0: runtime degree.
 template <int KIND, int M>
-__global__ void __launch_bounds__(kThreads) k_far_fast(EvalArgs a) {
+__global__ void __launch_bounds__(kWarps * 32)
+k_far_fast(EvalArgs a, const int2* __restrict__ items, int n_items, int* counter) {
   extern __shared__ double smem[];
   const int m = M > 0 ? M : a.degree + 1;
   const int m3 = m * m * m;
-  double* pts = smem;              // [3][kMaxM]
-  double* qh = smem + 3 * kMaxM;   // [m3]
-  const int b = a.work ? a.work[blockIdx.x] : blockIdx.x;
-  const int t0 = a.bstart[b], t1 = a.bstop[b];
-  const int e0 = a.a_ptr[(int64_t)b * a.G], e1 = a.a_ptr[(int64_t)(b + 1) * a.G];
-  for (int pass0 = t0; pass0 < t1; pass0 += kPass) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int per_warp = 3 * kMaxM + 1 + a.mstride;   // +1 keeps qh 16-byte aligned
+  double* pts = smem + warp * per_warp;   // [3][kMaxM]
+  double* qh = pts + 3 * kMaxM + 1;       // [mstride]
+  for (int item = next_item(counter); item < n_items; item = next_item(counter)) {
+    const int2 it = items[item];
+    const int b = it.x;
+    const int t1 = a.bstop[b];
     double tx[kTpt], ty[kTpt], tz[kTpt], acc[kTpt];
 #pragma unroll
     for (int k = 0; k < kTpt; ++k) {
-      const int i = min(pass0 + k * kThreads + (int)threadIdx.x, t1 - 1);
+      const int i = min(it.y + k * 32 + lane, t1 - 1);
       tx[k] = a.tx[i];
       ty[k] = a.ty[i];
       tz[k] = a.tz[i];
       acc[k] = 0.0;
     }
+    const int e0 = a.a_ptr[(int64_t)b * a.G], e1 = a.a_ptr[(int64_t)(b + 1) * a.G];
     for (int e = e0; e < e1; ++e) {
-      const EvalCluster c = a.clusters[a.a_idx[e]];
-      __syncthreads();
-      for (int i = threadIdx.x; i < 3 * m; i += kThreads) {
+      const EvalCluster* c = a.clusters + a.a_idx[e];
+      const double* row = a.moments + (size_t)c->mrow * a.mstride;
+      __syncwarp();
+      for (int i = lane; 2 * i < m3; i += 32) cp_async16(qh + 2 * i, row + 2 * i);
+      cp_async_commit();
+      for (int i = lane; i < 3 * m; i += 32) {
         const int d = i / m, k = i % m;
-        pts[d * kMaxM + k] = cheb_point_dev(a.degree, k, c.lo[d], c.hi[d], a.s_nodes);
+        pts[d * kMaxM + k] = cheb_point_dev(a.degree, k, c->lo[d], c->hi[d], a.s_nodes);
       }
-      const double* row = a.moments + (size_t)c.mrow * m3;
-      for (int i = threadIdx.x; i < m3; i += kThreads) qh[i] = row[i];
-      __syncthreads();
+      cp_async_wait<0>();
+      __syncwarp();
       if (KIND == 2) {
         double s = 0.0;
         for (int i = 0; i < m3; ++i) s = __dadd_rn(s, qh[i]);
@@ -107,6 +127,7 @@ __global__ void __launch_bounds__(kThreads) k_far_fast(EvalArgs a) {
             dz2[k][k3] = __dmul_rn(dz, dz);
           }
         }
+        const double* qr = qh;
         for (int k1 = 0; k1 < M; ++k1) {
           const double p1 = pts[k1];
           double dx2[kTpt];
@@ -115,7 +136,8 @@ __global__ void __launch_bounds__(kThreads) k_far_fast(EvalArgs a) {
             const double dx = __dsub_rn(tx[k], p1);
             dx2[k] = __dmul_rn(dx, dx);
           }
-          for (int k2 = 0; k2 < M; ++k2) {
+#pragma unroll 1
+          for (int k2 = 0; k2 < M; ++k2, qr += M) {
             const double p2 = pts[kMaxM + k2];
             double dxy2[kTpt];
 #pragma unroll
@@ -123,13 +145,12 @@ __global__ void __launch_bounds__(kThreads) k_far_fast(EvalArgs a) {
               const double dy = __dsub_rn(ty[k], p2);
               dxy2[k] = fma(dy, dy, dx2[k]);
             }
-            const double* qr = qh + (k1 * M + k2) * M;
 #pragma unroll
             for (int k3 = 0; k3 < M; ++k3) {
               const double qv = qr[k3];
 #pragma unroll
               for (int k = 0; k < kTpt; ++k)
-                acc[k] = far_accum<KIND>(acc[k], qv, __dadd_rn(dxy2[k], dz2[k][k3]), a.kappa);
+                acc[k] = far_term<KIND>(acc[k], qv, __dadd_rn(dxy2[k], dz2[k][k3]), a.kappa);
             }
           }
         }
@@ -152,7 +173,7 @@ __global__ void __launch_bounds__(kThreads) k_far_fast(EvalArgs a) {
 #pragma unroll
               for (int k = 0; k < kTpt; ++k) {
                 const double dz = __dsub_rn(tz[k], p3);
-                acc[k] = far_accum<KIND>(acc[k], qv, fma(dz, dz, dxy2[k]), a.kappa);
+                acc[k] = far_term<KIND>(acc[k], qv, fma(dz, dz, dxy2[k]), a.kappa);
               }
             }
           }
@@ -161,45 +182,71 @@ __global__ void __launch_bounds__(kThreads) k_far_fast(EvalArgs a) {
     }
 #pragma unroll
     for (int k = 0; k < kTpt; ++k) {
-      const int i = pass0 + k * kThreads + threadIdx.x;
+      const int i = it.y + k * 32 + lane;
       if (i < t1) a.far_out[i] = acc[k];
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// Near field: stream every direct cluster's sources through shared memory.
+// Near field: each direct cluster's sources stream through a double-buffered
+// per-warp stage of kSrcChunk packed (x, y, z, q) records.
+__device__ __forceinline__ void stage_sources(double4* dst, const double4* src, int base,
+                                              int stop, int lane) {
+  for (int jj = lane; jj < kSrcChunk; jj += 32) {
+    const int js = base + jj;
+    if (js < stop) {
+      cp_async16(&dst[jj], &src[js]);
+      cp_async16(reinterpret_cast<char*>(&dst[jj]) + 16,
+                 reinterpret_cast<const char*>(&src[js]) + 16);
+    }
+  }
+  cp_async_commit();
+}
+
 template <int KIND>
-__global__ void __launch_bounds__(kThreads) k_near_fast(EvalArgs a) {
-  __shared__ double4 tile[kSrcTile];
-  const int b = a.work ? a.work[blockIdx.x] : blockIdx.x;
-  const int t0 = a.bstart[b], t1 = a.bstop[b];
-  const int e0 = a.d_ptr[(int64_t)b * a.G], e1 = a.d_ptr[(int64_t)(b + 1) * a.G];
-  const long long tb = thr_bits();
-  for (int pass0 = t0; pass0 < t1; pass0 += kPass) {
+__global__ void __launch_bounds__(kWarps * 32)
+k_near_fast(EvalArgs a, const int2* __restrict__ items, int n_items, int* counter) {
+  __shared__ __align__(16) double4 stage[kWarps][2][kSrcChunk];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long tb = __double_as_longlong(kSingularSq);   // d2 >= 0: bit order = value order
+  for (int item = next_item(counter); item < n_items; item = next_item(counter)) {
+    const int2 it = items[item];
+    const int b = it.x;
+    const int t1 = a.bstop[b];
     double tx[kTpt], ty[kTpt], tz[kTpt], acc[kTpt], comp[kTpt];
 #pragma unroll
     for (int k = 0; k < kTpt; ++k) {
-      const int i = min(pass0 + k * kThreads + (int)threadIdx.x, t1 - 1);
+      const int i = min(it.y + k * 32 + lane, t1 - 1);
       tx[k] = a.tx[i];
       ty[k] = a.ty[i];
       tz[k] = a.tz[i];
       acc[k] = 0.0;
       comp[k] = 0.0;
     }
+    const int e0 = a.d_ptr[(int64_t)b * a.G], e1 = a.d_ptr[(int64_t)(b + 1) * a.G];
     for (int e = e0; e < e1; ++e) {
       const EvalCluster c = a.clusters[a.d_idx[e]];
-      for (int j0 = c.start; j0 < c.stop; j0 += kSrcTile) {
-        const int jn = min(kSrcTile, c.stop - j0);
-        __syncthreads();
-        for (int i = threadIdx.x; i < jn; i += kThreads) tile[i] = a.src4[j0 + i];
-        __syncthreads();
+      const int nchunks = (c.stop - c.start + kSrcChunk - 1) / kSrcChunk;
+      __syncwarp();
+      stage_sources(stage[warp][0], a.src4, c.start, c.stop, lane);
+      for (int ch = 0; ch < nchunks; ++ch) {
+        const int buf = ch & 1;
+        if (ch + 1 < nchunks) {
+          stage_sources(stage[warp][buf ^ 1], a.src4, c.start + (ch + 1) * kSrcChunk, c.stop,
+                        lane);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        __syncwarp();
+        const int jn = min(kSrcChunk, c.stop - (c.start + ch * kSrcChunk));
         double part[kTpt];
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) part[k] = 0.0;
-#pragma unroll 2
+#pragma unroll 4
         for (int j = 0; j < jn; ++j) {
-          const double4 s = tile[j];
+          const double4 s = stage[warp][buf][j];
 #pragma unroll
           for (int k = 0; k < kTpt; ++k) {
             const double dx = __dsub_rn(tx[k], s.x);
@@ -222,16 +269,16 @@ __global__ void __launch_bounds__(kThreads) k_near_fast(EvalArgs a) {
         }
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) neumaier(acc[k], comp[k], part[k]);
+        __syncwarp();
       }
     }
 #pragma unroll
     for (int k = 0; k < kTpt; ++k) {
-      const int i = pass0 + k * kThreads + threadIdx.x;
+      const int i = it.y + k * 32 + lane;
       if (i < t1) {
-        // far + near: the reference adds the approximations first, then the
-        // compensated direct sums on top (engine.py:302-312, 335).
-        double total = acc[k];
-        double cmp = comp[k];
+        // approximations first, then the compensated direct sums on top
+        // (engine.py:302-312, 335)
+        double total = acc[k], cmp = comp[k];
         neumaier(total, cmp, a.far_out[i]);
         a.out[i] = __dadd_rn(total, cmp);
       }
@@ -239,49 +286,100 @@ __global__ void __launch_bounds__(kThreads) k_near_fast(EvalArgs a) {
   }
 }
 
+__global__ void k_count_chunks(int64_t nb, const int32_t* bstart, const int32_t* bstop,
+                               int32_t* cnt) {
+  int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b < nb) cnt[b] = (bstop[b] - bstart[b] + kChunkT - 1) / kChunkT;
+  if (b == nb) cnt[b] = 0;
+}
+
+__global__ void k_fill_items(int64_t nb, const int32_t* bstart, const int32_t* cnt,
+                             const int32_t* off, int2* items) {
+  int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  for (int k = 0; k < cnt[b]; ++k) items[off[b] + k] = make_int2((int)b, bstart[b] + k * kChunkT);
+}
+
+template <typename K>
+int persistent_grid(K kernel, int threads, size_t smem) {
+  int dev = 0, sms = 0, per_sm = 0;
+  BLTC_CUDA(cudaGetDevice(&dev));
+  BLTC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  BLTC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+  return sms * (per_sm > 0 ? per_sm : 1);
+}
+
 template <int KIND, int M>
-void far_launch(const EvalArgs& a, cudaStream_t st) {
-  const int m = M > 0 ? M : a.degree + 1;
-  const size_t smem = sizeof(double) * (3 * kMaxM + (size_t)m * m * m);
-  BLTC_CUDA(cudaFuncSetAttribute(k_far_fast<KIND, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-  k_far_fast<KIND, M><<<(unsigned)a.nb, kThreads, smem, st>>>(a);
+void far_launch(const EvalArgs& a, const int2* items, int n_items, int* counter,
+                cudaStream_t st) {
+  const size_t smem = sizeof(double) * kWarps * (3 * kMaxM + 1 + (size_t)a.mstride);
+  auto kern = k_far_fast<KIND, M>;
+  BLTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = persistent_grid(kern, kWarps * 32, smem);
+  kern<<<grid, kWarps * 32, smem, st>>>(a, items, n_items, counter);
   BLTC_LAUNCH_CHECK();
 }
 
 template <int KIND>
-void far_dispatch(const EvalArgs& a, cudaStream_t st) {
+void far_dispatch(const EvalArgs& a, const int2* items, int n_items, int* counter,
+                  cudaStream_t st) {
   switch (a.degree + 1) {
-    case 5: far_launch<KIND, 5>(a, st); break;
-    case 6: far_launch<KIND, 6>(a, st); break;
-    case 8: far_launch<KIND, 8>(a, st); break;
-    case 9: far_launch<KIND, 9>(a, st); break;
-    case 11: far_launch<KIND, 11>(a, st); break;
-    default: far_launch<KIND, 0>(a, st); break;
+    case 5: far_launch<KIND, 5>(a, items, n_items, counter, st); break;
+    case 6: far_launch<KIND, 6>(a, items, n_items, counter, st); break;
+    case 8: far_launch<KIND, 8>(a, items, n_items, counter, st); break;
+    case 9: far_launch<KIND, 9>(a, items, n_items, counter, st); break;
+    case 11: far_launch<KIND, 11>(a, items, n_items, counter, st); break;
+    default: far_launch<KIND, 0>(a, items, n_items, counter, st); break;
   }
+}
+
+template <int KIND>
+void near_launch(const EvalArgs& a, const int2* items, int n_items, int* counter,
+                 cudaStream_t st) {
+  auto kern = k_near_fast<KIND>;
+  const int grid = persistent_grid(kern, kWarps * 32, 0);
+  kern<<<grid, kWarps * 32, 0, st>>>(a, items, n_items, counter);
+  BLTC_LAUNCH_CHECK();
 }
 }  // namespace
 
-void launch_eval_fast(const EvalArgs& a, int kind, cudaStream_t st, cudaStream_t st2,
-                      cudaEvent_t far_done, float* far_ms, float* near_ms, bool timing) {
-  (void)st2;
-  (void)far_done;
-  if (a.nb == 0) return;
+void build_fast_items(const EvalArgs& a, DBuf<int32_t>& cnt, DBuf<int32_t>& off,
+                      DBuf<int2>& items, DBuf<int32_t>& scan_tmp, HostScratch& hs,
+                      cudaStream_t st, int* n_items) {
+  const int64_t nb = a.nb;
+  cnt.resize(nb + 1);
+  off.resize(nb + 1);
+  k_count_chunks<<<(int)((nb + 1 + 255) / 256), 256, 0, st>>>(nb, a.bstart, a.bstop, cnt.p);
+  BLTC_LAUNCH_CHECK();
+  exclusive_scan_i32(cnt.p, off.p, nb + 1, scan_tmp, st);
+  int32_t* h = (int32_t*)hs.get(64);
+  BLTC_CUDA(cudaMemcpyAsync(h, off.p + nb, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  BLTC_CUDA(cudaStreamSynchronize(st));
+  *n_items = h[0];
+  items.resize(*n_items + 1);
+  k_fill_items<<<(int)((nb + 255) / 256), 256, 0, st>>>(nb, a.bstart, cnt.p, off.p, items.p);
+  BLTC_LAUNCH_CHECK();
+}
+
+void launch_eval_fast(const EvalArgs& a, int kind, const int2* items, int n_items,
+                      int* counters, cudaStream_t st, float* far_ms, float* near_ms,
+                      bool timing) {
+  if (a.nb == 0 || n_items == 0) return;
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
   if (timing) {
     BLTC_CUDA(cudaEventCreate(&e0));
     BLTC_CUDA(cudaEventCreate(&e1));
     BLTC_CUDA(cudaEventCreate(&e2));
-    BLTC_CUDA(cudaEventRecord(e0, st));
   }
-  if (kind == 0) far_dispatch<0>(a, st);
-  else if (kind == 1) far_dispatch<1>(a, st);
-  else far_launch<2, 0>(a, st);
+  BLTC_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int), st));
+  if (timing) BLTC_CUDA(cudaEventRecord(e0, st));
+  if (kind == 0) far_dispatch<0>(a, items, n_items, counters, st);
+  else if (kind == 1) far_dispatch<1>(a, items, n_items, counters, st);
+  else far_launch<2, 0>(a, items, n_items, counters, st);
   if (timing) BLTC_CUDA(cudaEventRecord(e1, st));
-  if (kind == 0) k_near_fast<0><<<(unsigned)a.nb, kThreads, 0, st>>>(a);
-  else if (kind == 1) k_near_fast<1><<<(unsigned)a.nb, kThreads, 0, st>>>(a);
-  else k_near_fast<2><<<(unsigned)a.nb, kThreads, 0, st>>>(a);
-  BLTC_LAUNCH_CHECK();
+  if (kind == 0) near_launch<0>(a, items, n_items, counters + 1, st);
+  else if (kind == 1) near_launch<1>(a, items, n_items, counters + 1, st);
+  else near_launch<2>(a, items, n_items, counters + 1, st);
   if (timing) {
     BLTC_CUDA(cudaEventRecord(e2, st));
     BLTC_CUDA(cudaEventSynchronize(e2));

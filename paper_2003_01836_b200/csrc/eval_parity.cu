@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(kThreads) k_eval_parity(EvalArgs a) {
           int d = i / m, k = i % m;
           pts[d * kMaxM + k] = cheb_point_dev(a.degree, k, c.lo[d], c.hi[d], a.s_nodes);
         }
-        const double* row = a.moments + (size_t)c.mrow * m3;
+        const double* row = a.moments + (size_t)c.mrow * a.mstride;
         for (int i = threadIdx.x; i < m3; i += kThreads) qh[i] = row[i];
         __syncthreads();
 #pragma unroll
@@ -146,19 +146,21 @@ void launch_eval_parity(const EvalArgs& a, int kind, cudaStream_t st) {
       BLTC_CUDA(cudaFuncSetAttribute(k_eval_parity<0>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       k_eval_parity<0><<<(unsigned)a.nb, kThreads, smem, st>>>(a);
+      BLTC_LAUNCH_CHECK();
       break;
     case 1:
       BLTC_CUDA(cudaFuncSetAttribute(k_eval_parity<1>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       k_eval_parity<1><<<(unsigned)a.nb, kThreads, smem, st>>>(a);
+      BLTC_LAUNCH_CHECK();
       break;
     default:
       BLTC_CUDA(cudaFuncSetAttribute(k_eval_parity<2>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       k_eval_parity<2><<<(unsigned)a.nb, kThreads, smem, st>>>(a);
+      BLTC_LAUNCH_CHECK();
       break;
   }
-  BLTC_LAUNCH_CHECK();
 }
 
 }  // namespace bltc

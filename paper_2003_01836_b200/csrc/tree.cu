@@ -454,14 +454,14 @@ void build_partition(Partition& P, BuildScratch& S, int64_t n, const double* dx,
     S.box_u.grow_keep(6 * c, st);
   };
   P.n_nodes = 0;
-  P.start.release(); P.stop.release(); P.child_start.release(); P.child_count.release();
-  P.level.release(); P.lo.release(); P.hi.release(); S.box_u.release();
   ensure_nodes(cap);
   P.n_nodes = 1;
   k_root<<<1, 1, 0, st>>>(P.start.p, P.stop.p, P.level.p, n);
   BLTC_LAUNCH_CHECK();
   k_init_boxes<<<1, 32, 0, st>>>(S.box_u.p, 0, 1);
+  BLTC_LAUNCH_CHECK();
   k_box<<<std::min(grid_for(n, 256), 148 * 8), 256, 0, st>>>(n, cx, cy, cz, cn, S.box_u.p);
+  BLTC_LAUNCH_CHECK();
   k_finalize_boxes<<<1, 32, 0, st>>>(S.box_u.p, P.lo.p, P.hi.p, 0, 1);
   BLTC_LAUNCH_CHECK();
 
@@ -507,7 +507,9 @@ void build_partition(Partition& P, BuildScratch& S, int64_t n, const double* dx,
     std::swap(co, no); std::swap(cn, nn_);
     const int64_t nb = end, ne = end + total_children;
     k_init_boxes<<<grid_for(ne - nb, 128), 128, 0, st>>>(S.box_u.p, nb, ne);
+    BLTC_LAUNCH_CHECK();
     k_box<<<std::min(grid_for(n, 256), 148 * 8), 256, 0, st>>>(n, cx, cy, cz, cn, S.box_u.p);
+    BLTC_LAUNCH_CHECK();
     k_finalize_boxes<<<grid_for(ne - nb, 128), 128, 0, st>>>(S.box_u.p, P.lo.p, P.hi.p, nb, ne);
     BLTC_LAUNCH_CHECK();
     P.n_nodes = ne;

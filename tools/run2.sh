@@ -1,0 +1,4 @@
+timeout 600 python -m pytest tests -x -q -m gpu > gpurun_out/gpu_tests.log 2>&1; tail -3 gpurun_out/gpu_tests.log
+timeout 300 python bench.py --config c4 --steps 3 --no-cpu-baseline > gpurun_out/b_c4.json 2> gpurun_out/b_c4.err
+timeout 300 python bench.py --config c4 --steps 3 --batch-size 1000 --no-cpu-baseline > gpurun_out/b_c4_nb1000.json 2> gpurun_out/b_c4_nb1000.err
+timeout 300 python bench.py --config c2 --steps 3 --no-cpu-baseline > gpurun_out/b_c2.json 2> gpurun_out/b_c2.err
