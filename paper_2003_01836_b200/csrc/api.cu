@@ -167,7 +167,7 @@ struct bltc_ctx {
   DBuf<double> out_sorted, far_out, phi_dev;
   DBuf<double4> src4;
   DBuf<int32_t> item_cnt, item_off, counters;
-  DBuf<int2> items;
+  DBuf<int2> items, items2;
   DBuf<double> partial;
   DBuf<int32_t> flag;
   DBuf<int64_t> widen;
@@ -439,12 +439,22 @@ void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, 
     c->far_out.resize(T.n);
     a.far_out = c->far_out.p;
     float far_ms = 0, near_ms = 0;
-    int n_items = 0;
-    build_fast_items(a, c->item_cnt, c->item_off, c->items, c->bs.scan_tmp, c->hs, st,
-                     &n_items);
+    const FastTuning tune = fast_tuning();
+    const bool tuned = p->kernel_code == 0;
+    const int far_chunk = 32 * (tuned && p->degree == 8 ? tune.far_tpt : 2);
+    const int near_chunk = 32 * (tuned ? tune.near_tpt : 2);
+    FastItems fi, ni;
+    build_fast_items(a, far_chunk, c->item_cnt, c->item_off, c->items, c->bs.scan_tmp, c->hs,
+                     st, &fi);
+    if (near_chunk == far_chunk) {
+      ni = fi;
+    } else {
+      build_fast_items(a, near_chunk, c->item_cnt, c->item_off, c->items2, c->bs.scan_tmp,
+                       c->hs, st, &ni);
+    }
     c->counters.resize(2);
-    launch_eval_fast(a, p->kernel_code, c->items.p, n_items, c->counters.p, st, &far_ms,
-                     &near_ms, c->timing);
+    launch_eval_fast(a, p->kernel_code, fi, ni, tune, c->counters.p, st, &far_ms, &near_ms,
+                     c->timing);
     if (stats) {
       stats->far_s = far_ms * 1e-3;
       stats->near_s = near_ms * 1e-3;
@@ -636,7 +646,7 @@ int bltc_destroy(bltc_ctx* c) {
     c->rows.release(); c->s_nodes.release(); c->w_nodes.release(); c->out_sorted.release();
     c->far_out.release(); c->phi_dev.release(); c->src4.release(); c->flag.release();
     c->widen.release(); c->item_cnt.release(); c->item_off.release(); c->counters.release();
-    c->items.release(); c->partial.release(); c->f_ecl.release(); c->f_mac.release(); c->f_x.release();
+    c->items.release(); c->items2.release(); c->partial.release(); c->f_ecl.release(); c->f_mac.release(); c->f_x.release();
     c->f_y.release(); c->f_z.release(); c->f_q.release(); c->f_rows.release();
     c->f_src4.release();
     c->hs.release();

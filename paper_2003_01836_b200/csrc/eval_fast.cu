@@ -21,11 +21,12 @@
 #include "bltc_internal.cuh"
 #include "eval_common.cuh"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace bltc {
 
 namespace {
-constexpr int kTpt = 2;                 // targets per lane
-constexpr int kChunkT = 32 * kTpt;      // targets per work item
 constexpr int kWarps = 8;               // warps per CTA
 constexpr int kSrcChunk = 64;           // near-field sources per stage
 
@@ -63,18 +64,54 @@ __device__ __forceinline__ int next_item(int* counter) {
   return __shfl_sync(0xffffffffu, it, 0);
 }
 
-template <int KIND>
-__device__ __forceinline__ double far_term(double acc, double qv, double d2, double kappa) {
-  if (KIND == 0) return fma(qv, rsqrt_fast(d2), acc);
-  const double y = rsqrt_fast(d2);
-  const double r = __dmul_rn(d2, y);
-  return fma(__dmul_rn(qv, exp(-kappa * r)), y, acc);
+
+// q / sqrt(d2) accumulated into acc, full double accuracy, in the form that
+// keeps 3-register-operand DFMAs (which issue at 2/3 rate on sm_100a: the
+// register file delivers two 64-bit operands per cycle) to one per pair:
+//   y0 = MUFU.RSQ64H(d2); e = 1 - d2 y0^2; p = 1 + e (1/2 + 3/8 e)
+//   acc += (q y0) p                                  (cubic, error O(e^3))
+// FORM 1 splits the last FMA into DMUL + DADD (no 3-register DFMA at all).
+template <int FORM>
+__device__ __forceinline__ double coulomb_acc(double acc, double q, double d2) {
+  double y0;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(d2));
+  const double e = fma(-__dmul_rn(d2, y0), y0, 1.0);
+  const double c = fma(0.375, e, 0.5);
+  const double p = fma(e, c, 1.0);
+  const double qy = __dmul_rn(q, y0);
+  if (FORM == 1) return __dadd_rn(acc, __dmul_rn(qy, p));
+  return fma(qy, p, acc);
+}
+
+template <int KIND, int FORM>
+__device__ __forceinline__ double pair_acc(double acc, double q, double d2, double kappa) {
+  if (KIND == 0) return coulomb_acc<FORM>(acc, q, d2);
+  if (KIND == 1) {
+    const double y = rsqrt_fast(d2);
+    const double r = __dmul_rn(d2, y);
+    return fma(__dmul_rn(q, exp(-kappa * r)), y, acc);
+  }
+  return __dadd_rn(acc, q);
+}
+
+// One (k1, k2) row of the proxy grid against kTpt targets.
+template <int KIND, int M, int kTpt, int FORM>
+__device__ __forceinline__ void far_row(double (&acc)[kTpt], const double* qr,
+                                        const double (&dxy2)[kTpt],
+                                        const double (&dz2)[kTpt][M], double kappa) {
+#pragma unroll
+  for (int k3 = 0; k3 < M; ++k3) {
+    const double qv = qr[k3];
+#pragma unroll
+    for (int k = 0; k < kTpt; ++k)
+      acc[k] = pair_acc<KIND, FORM>(acc[k], qv, __dadd_rn(dxy2[k], dz2[k][k3]), kappa);
+  }
 }
 
 // ---------------------------------------------------------------------------
 // Far field.  M = n + 1 at compile time (k3 unrolled); M = 0: runtime degree.
-template <int KIND, int M>
-__global__ void __launch_bounds__(kWarps * 32)
+template <int KIND, int M, int kTpt, int MINB, int FORM>
+__global__ void __launch_bounds__(kWarps * 32, MINB)
 k_far_fast(EvalArgs a, const int2* __restrict__ items, int n_items, int* counter) {
   extern __shared__ double smem[];
   const int m = M > 0 ? M : a.degree + 1;
@@ -116,7 +153,7 @@ k_far_fast(EvalArgs a, const int2* __restrict__ items, int n_items, int* counter
         for (int k = 0; k < kTpt; ++k) acc[k] = __dadd_rn(acc[k], s);
         continue;
       }
-      if (M > 0) {
+      if constexpr (M > 0) {
         double dz2[kTpt][M > 0 ? M : 1];
 #pragma unroll
         for (int k3 = 0; k3 < M; ++k3) {
@@ -145,13 +182,7 @@ k_far_fast(EvalArgs a, const int2* __restrict__ items, int n_items, int* counter
               const double dy = __dsub_rn(ty[k], p2);
               dxy2[k] = fma(dy, dy, dx2[k]);
             }
-#pragma unroll
-            for (int k3 = 0; k3 < M; ++k3) {
-              const double qv = qr[k3];
-#pragma unroll
-              for (int k = 0; k < kTpt; ++k)
-                acc[k] = far_term<KIND>(acc[k], qv, __dadd_rn(dxy2[k], dz2[k][k3]), a.kappa);
-            }
+            far_row<KIND, M, kTpt, FORM>(acc, qr, dxy2, dz2, a.kappa);
           }
         }
       } else {
@@ -173,7 +204,7 @@ k_far_fast(EvalArgs a, const int2* __restrict__ items, int n_items, int* counter
 #pragma unroll
               for (int k = 0; k < kTpt; ++k) {
                 const double dz = __dsub_rn(tz[k], p3);
-                acc[k] = far_term<KIND>(acc[k], qv, fma(dz, dz, dxy2[k]), a.kappa);
+                acc[k] = pair_acc<KIND, FORM>(acc[k], qv, fma(dz, dz, dxy2[k]), a.kappa);
               }
             }
           }
@@ -204,8 +235,8 @@ __device__ __forceinline__ void stage_sources(double4* dst, const double4* src, 
   cp_async_commit();
 }
 
-template <int KIND>
-__global__ void __launch_bounds__(kWarps * 32)
+template <int KIND, int kTpt, int MINB, int FORM>
+__global__ void __launch_bounds__(kWarps * 32, MINB)
 k_near_fast(EvalArgs a, const int2* __restrict__ items, int n_items, int* counter) {
   __shared__ __align__(16) double4 stage[kWarps][2][kSrcChunk];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -256,15 +287,7 @@ k_near_fast(EvalArgs a, const int2* __restrict__ items, int n_items, int* counte
             const bool ok = __double_as_longlong(d2) >= tb;
             const double d2s = ok ? d2 : 1.0;
             const double qs = ok ? s.w : 0.0;
-            if (KIND == 0) {
-              part[k] = fma(qs, rsqrt_fast(d2s), part[k]);
-            } else if (KIND == 1) {
-              const double y = rsqrt_fast(d2s);
-              const double r = __dmul_rn(d2s, y);
-              part[k] = fma(__dmul_rn(qs, exp(-a.kappa * r)), y, part[k]);
-            } else {
-              part[k] = __dadd_rn(part[k], qs);
-            }
+            part[k] = pair_acc<KIND, FORM>(part[k], qs, d2s, a.kappa);
           }
         }
 #pragma unroll
@@ -287,14 +310,14 @@ k_near_fast(EvalArgs a, const int2* __restrict__ items, int n_items, int* counte
 }
 
 __global__ void k_count_chunks(int64_t nb, const int32_t* bstart, const int32_t* bstop,
-                               int32_t* cnt) {
+                               int kChunkT, int32_t* cnt) {
   int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (b < nb) cnt[b] = (bstop[b] - bstart[b] + kChunkT - 1) / kChunkT;
   if (b == nb) cnt[b] = 0;
 }
 
 __global__ void k_fill_items(int64_t nb, const int32_t* bstart, const int32_t* cnt,
-                             const int32_t* off, int2* items) {
+                             const int32_t* off, int kChunkT, int2* items) {
   int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (b >= nb) return;
   for (int k = 0; k < cnt[b]; ++k) items[off[b] + k] = make_int2((int)b, bstart[b] + k * kChunkT);
@@ -309,62 +332,103 @@ int persistent_grid(K kernel, int threads, size_t smem) {
   return sms * (per_sm > 0 ? per_sm : 1);
 }
 
-template <int KIND, int M>
-void far_launch(const EvalArgs& a, const int2* items, int n_items, int* counter,
-                cudaStream_t st) {
+template <int KIND, int M, int TPT, int MINB, int FORM = 0>
+void far_launch(const EvalArgs& a, const FastItems& it, int* counter, cudaStream_t st) {
   const size_t smem = sizeof(double) * kWarps * (3 * kMaxM + 1 + (size_t)a.mstride);
-  auto kern = k_far_fast<KIND, M>;
+  auto kern = k_far_fast<KIND, M, TPT, MINB, FORM>;
   BLTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = persistent_grid(kern, kWarps * 32, smem);
-  kern<<<grid, kWarps * 32, smem, st>>>(a, items, n_items, counter);
+  kern<<<grid, kWarps * 32, smem, st>>>(a, it.items, it.n_items, counter);
   BLTC_LAUNCH_CHECK();
 }
 
+// Tuned variants exist for the benchmark shape (Coulomb, n = 8); every other
+// (kernel, degree) uses (kTpt, minBlocks) = (2, 2).
+template <int KIND, int M>
+void far_variant(const EvalArgs& a, const FastItems& it, int* counter, cudaStream_t st,
+                 const FastTuning& t) {
+  if (KIND == 0 && M == 9) {
+    if (t.far_tpt == 1 && t.far_minb == 4) return far_launch<KIND, M, 1, 4>(a, it, counter, st);
+    if (t.far_tpt == 2 && t.far_minb == 3) return far_launch<KIND, M, 2, 3>(a, it, counter, st);
+    if (t.far_tpt == 4 && t.far_minb == 2) return far_launch<KIND, M, 4, 2>(a, it, counter, st);
+    if (t.far_tpt == 3 && t.far_minb == 2) return far_launch<KIND, M, 3, 2>(a, it, counter, st);
+    if (t.far_tpt == 2 && t.far_minb == 2 && t.form == 1)
+      return far_launch<KIND, M, 2, 2, 1>(a, it, counter, st);
+  }
+  far_launch<KIND, M, 2, 2>(a, it, counter, st);
+}
+
 template <int KIND>
-void far_dispatch(const EvalArgs& a, const int2* items, int n_items, int* counter,
-                  cudaStream_t st) {
+void far_dispatch(const EvalArgs& a, const FastItems& it, int* counter, cudaStream_t st,
+                  const FastTuning& t) {
   switch (a.degree + 1) {
-    case 5: far_launch<KIND, 5>(a, items, n_items, counter, st); break;
-    case 6: far_launch<KIND, 6>(a, items, n_items, counter, st); break;
-    case 8: far_launch<KIND, 8>(a, items, n_items, counter, st); break;
-    case 9: far_launch<KIND, 9>(a, items, n_items, counter, st); break;
-    case 11: far_launch<KIND, 11>(a, items, n_items, counter, st); break;
-    default: far_launch<KIND, 0>(a, items, n_items, counter, st); break;
+    case 5: far_variant<KIND, 5>(a, it, counter, st, t); break;
+    case 6: far_variant<KIND, 6>(a, it, counter, st, t); break;
+    case 8: far_variant<KIND, 8>(a, it, counter, st, t); break;
+    case 9: far_variant<KIND, 9>(a, it, counter, st, t); break;
+    case 11: far_variant<KIND, 11>(a, it, counter, st, t); break;
+    default: far_launch<KIND, 0, 2, 2>(a, it, counter, st); break;
   }
 }
 
-template <int KIND>
-void near_launch(const EvalArgs& a, const int2* items, int n_items, int* counter,
-                 cudaStream_t st) {
-  auto kern = k_near_fast<KIND>;
+template <int KIND, int TPT, int MINB, int FORM = 0>
+void near_launch(const EvalArgs& a, const FastItems& it, int* counter, cudaStream_t st) {
+  auto kern = k_near_fast<KIND, TPT, MINB, FORM>;
   const int grid = persistent_grid(kern, kWarps * 32, 0);
-  kern<<<grid, kWarps * 32, 0, st>>>(a, items, n_items, counter);
+  kern<<<grid, kWarps * 32, 0, st>>>(a, it.items, it.n_items, counter);
   BLTC_LAUNCH_CHECK();
+}
+
+template <int KIND>
+void near_variant(const EvalArgs& a, const FastItems& it, int* counter, cudaStream_t st,
+                  const FastTuning& t) {
+  if (KIND == 0) {
+    if (t.near_tpt == 1 && t.near_minb == 4) return near_launch<KIND, 1, 4>(a, it, counter, st);
+    if (t.near_tpt == 2 && t.near_minb == 3) return near_launch<KIND, 2, 3>(a, it, counter, st);
+    if (t.near_tpt == 2 && t.near_minb == 4) return near_launch<KIND, 2, 4>(a, it, counter, st);
+    if (t.near_tpt == 4 && t.near_minb == 2) return near_launch<KIND, 4, 2>(a, it, counter, st);
+    if (t.near_tpt == 2 && t.near_minb == 2 && t.form == 1)
+      return near_launch<KIND, 2, 2, 1>(a, it, counter, st);
+  }
+  near_launch<KIND, 2, 2>(a, it, counter, st);
 }
 }  // namespace
 
-void build_fast_items(const EvalArgs& a, DBuf<int32_t>& cnt, DBuf<int32_t>& off,
+FastTuning fast_tuning() {
+  FastTuning t{2, 2, 2, 2, 0};
+  if (const char* e = std::getenv("BLTC_FORM")) t.form = std::atoi(e);
+  if (const char* e = std::getenv("BLTC_FAR")) std::sscanf(e, "%d,%d", &t.far_tpt, &t.far_minb);
+  if (const char* e = std::getenv("BLTC_NEAR"))
+    std::sscanf(e, "%d,%d", &t.near_tpt, &t.near_minb);
+  return t;
+}
+
+void build_fast_items(const EvalArgs& a, int chunk, DBuf<int32_t>& cnt, DBuf<int32_t>& off,
                       DBuf<int2>& items, DBuf<int32_t>& scan_tmp, HostScratch& hs,
-                      cudaStream_t st, int* n_items) {
+                      cudaStream_t st, FastItems* out) {
   const int64_t nb = a.nb;
   cnt.resize(nb + 1);
   off.resize(nb + 1);
-  k_count_chunks<<<(int)((nb + 1 + 255) / 256), 256, 0, st>>>(nb, a.bstart, a.bstop, cnt.p);
+  k_count_chunks<<<(int)((nb + 1 + 255) / 256), 256, 0, st>>>(nb, a.bstart, a.bstop, chunk,
+                                                               cnt.p);
   BLTC_LAUNCH_CHECK();
   exclusive_scan_i32(cnt.p, off.p, nb + 1, scan_tmp, st);
   int32_t* h = (int32_t*)hs.get(64);
   BLTC_CUDA(cudaMemcpyAsync(h, off.p + nb, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   BLTC_CUDA(cudaStreamSynchronize(st));
-  *n_items = h[0];
-  items.resize(*n_items + 1);
-  k_fill_items<<<(int)((nb + 255) / 256), 256, 0, st>>>(nb, a.bstart, cnt.p, off.p, items.p);
+  out->n_items = h[0];
+  items.resize(out->n_items + 1);
+  k_fill_items<<<(int)((nb + 255) / 256), 256, 0, st>>>(nb, a.bstart, cnt.p, off.p, chunk,
+                                                        items.p);
   BLTC_LAUNCH_CHECK();
+  out->items = items.p;
+  out->chunk = chunk;
 }
 
-void launch_eval_fast(const EvalArgs& a, int kind, const int2* items, int n_items,
-                      int* counters, cudaStream_t st, float* far_ms, float* near_ms,
-                      bool timing) {
-  if (a.nb == 0 || n_items == 0) return;
+void launch_eval_fast(const EvalArgs& a, int kind, const FastItems& far_items,
+                      const FastItems& near_items, const FastTuning& t, int* counters,
+                      cudaStream_t st, float* far_ms, float* near_ms, bool timing) {
+  if (a.nb == 0) return;
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
   if (timing) {
     BLTC_CUDA(cudaEventCreate(&e0));
@@ -373,13 +437,13 @@ void launch_eval_fast(const EvalArgs& a, int kind, const int2* items, int n_item
   }
   BLTC_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int), st));
   if (timing) BLTC_CUDA(cudaEventRecord(e0, st));
-  if (kind == 0) far_dispatch<0>(a, items, n_items, counters, st);
-  else if (kind == 1) far_dispatch<1>(a, items, n_items, counters, st);
-  else far_launch<2, 0>(a, items, n_items, counters, st);
+  if (kind == 0) far_dispatch<0>(a, far_items, counters, st, t);
+  else if (kind == 1) far_dispatch<1>(a, far_items, counters, st, t);
+  else far_launch<2, 0, 2, 2>(a, far_items, counters, st);
   if (timing) BLTC_CUDA(cudaEventRecord(e1, st));
-  if (kind == 0) near_launch<0>(a, items, n_items, counters + 1, st);
-  else if (kind == 1) near_launch<1>(a, items, n_items, counters + 1, st);
-  else near_launch<2>(a, items, n_items, counters + 1, st);
+  if (kind == 0) near_variant<0>(a, near_items, counters + 1, st, t);
+  else if (kind == 1) near_launch<1, 2, 2>(a, near_items, counters + 1, st);
+  else near_launch<2, 2, 2>(a, near_items, counters + 1, st);
   if (timing) {
     BLTC_CUDA(cudaEventRecord(e2, st));
     BLTC_CUDA(cudaEventSynchronize(e2));

@@ -1,0 +1,4 @@
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_far_fast -c 1 -o gpurun_out/prof_far_c2 python tools/one_step.py --config c2 --steps 1 > gpurun_out/prof_far.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_near_fast -c 1 -o gpurun_out/prof_near_c2 python tools/one_step.py --config c2 --steps 1 > gpurun_out/prof_near.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_c4.csv python tools/one_step.py --config c4 --steps 2 > gpurun_out/launch_c4.log 2>&1
+ls -la gpurun_out
