@@ -141,49 +141,64 @@ def probe_fp64(device: int) -> float:
     return v.value
 
 
-def cpu_baseline(system, cfg, econf, budget_pairs: float = 1.5e10, threads: int | None = None):
-    """Oracle (C restatement of the reference path) on the host cores,
-    bounded: full tree / batches / lists / moments, evaluation on a random
-    sample of target batches, extrapolated by pair count."""
-    from oracle import oracle as orc
-    threads = threads or os.cpu_count() or 1
-    s = system.sources
-    t0 = time.perf_counter()
-    tree = orc.build_source_tree(s.x, s.y, s.z, system.charges, econf.leaf_size)
-    if econf.batch_size == econf.leaf_size:
-        lf = tree.leaf_dfs
-        batches = orc.Batches(tree=tree, start=tree.start[lf], stop=tree.stop[lf],
-                              center=tree.center[lf], radius=tree.radius[lf])
-    else:
-        batches = orc.build_target_batches(s.x, s.y, s.z, econf.batch_size)
-    lists = orc.build_lists(batches, tree, econf.theta, econf.degree)
-    t1 = time.perf_counter()
-    rows, mrow = orc.compute_moments(tree, econf.degree, np.unique(lists.a_idx), threads)
-    t2 = time.perf_counter()
-    nt = batches.stop - batches.start
-    m3 = (econf.degree + 1) ** 3
-    csum = np.concatenate([[0], np.cumsum(tree.count[lists.d_idx])])
-    dpairs = nt * (csum[lists.d_ptr[1:]] - csum[lists.d_ptr[:-1]])
-    apairs = nt * m3 * np.diff(lists.a_ptr)
-    cost = dpairs + apairs
-    rng = np.random.default_rng(0)
-    order = rng.permutation(batches.nb)
-    take = np.searchsorted(np.cumsum(cost[order]), budget_pairs) + 1
-    sel = np.sort(order[:min(take, batches.nb)])
-    frac = float(cost[sel].sum() / cost.sum())
-    t3 = time.perf_counter()
-    orc.evaluate(batches, [orc.SourceGroup(tree, rows, mrow, lists)], econf.degree,
-                 econf.kernel.code, econf.kernel.kappa, threads, sel=sel)
-    t4 = time.perf_counter()
-    est = (t1 - t0) + (t2 - t1) + (t4 - t3) / frac
-    return {"value": system.n_targets / est, "unit": "particles/s", "cores": threads,
-            "kind": "port",
-            "sample": (f"oracle/ C port of the reference path, {threads} threads: full tree+"
-                       f"batches+lists ({t1 - t0:.1f}s, serial) and moments ({t2 - t1:.1f}s), "
-                       f"evaluation of {len(sel)}/{batches.nb} random batches = {frac:.4f} of "
-                       f"the pairs in {t4 - t3:.1f}s, extrapolated: est {est:.1f}s per step"),
-            "est_step_s": est, "setup_s": t1 - t0, "moments_s": t2 - t1,
-            "eval_sample_s": t4 - t3, "sample_frac": frac}
+class CpuReference:
+    """The reference's CPU algorithm (oracle/: C restatement of the reference
+    path, "port") on this host's cores, on a bounded sample of the workload:
+    full tree / batches / lists / moments (timed once), then evaluation of a
+    random sample of target batches (timed per step), extrapolated to the
+    whole workload by pair count."""
+
+    def __init__(self, system, econf, budget_pairs: float = 1.5e10, threads: int | None = None):
+        from oracle import oracle as orc
+        self.orc = orc
+        self.threads = threads or os.cpu_count() or 1
+        self.system, self.econf = system, econf
+        s = system.sources
+        t0 = time.perf_counter()
+        tree = orc.build_source_tree(s.x, s.y, s.z, system.charges, econf.leaf_size)
+        if econf.batch_size == econf.leaf_size:
+            lf = tree.leaf_dfs
+            batches = orc.Batches(tree=tree, start=tree.start[lf], stop=tree.stop[lf],
+                                  center=tree.center[lf], radius=tree.radius[lf])
+        else:
+            batches = orc.build_target_batches(s.x, s.y, s.z, econf.batch_size)
+        lists = orc.build_lists(batches, tree, econf.theta, econf.degree)
+        t1 = time.perf_counter()
+        rows, mrow = orc.compute_moments(tree, econf.degree, np.unique(lists.a_idx),
+                                         self.threads)
+        t2 = time.perf_counter()
+        self.setup_s, self.moments_s = t1 - t0, t2 - t1
+        self.tree, self.batches, self.lists, self.rows, self.mrow = tree, batches, lists, rows, mrow
+        nt = batches.stop - batches.start
+        m3 = (econf.degree + 1) ** 3
+        csum = np.concatenate([[0], np.cumsum(tree.count[lists.d_idx])])
+        cost = nt * (csum[lists.d_ptr[1:]] - csum[lists.d_ptr[:-1]]) + nt * m3 * np.diff(lists.a_ptr)
+        order = np.random.default_rng(0).permutation(batches.nb)
+        take = int(np.searchsorted(np.cumsum(cost[order]), budget_pairs)) + 1
+        self.sel = np.sort(order[:min(take, batches.nb)])
+        self.frac = float(cost[self.sel].sum() / cost.sum())
+
+    def step(self) -> dict:
+        t0 = time.perf_counter()
+        self.orc.evaluate(self.batches, [self.orc.SourceGroup(self.tree, self.rows, self.mrow,
+                                                               self.lists)],
+                          self.econf.degree, self.econf.kernel.code, self.econf.kernel.kappa,
+                          self.threads, sel=self.sel)
+        t = time.perf_counter() - t0
+        est = self.setup_s + self.moments_s + t / self.frac
+        return {"value": self.system.n_targets / est, "unit": "particles/s",
+                "cores": self.threads, "kind": "port",
+                "sample": (f"oracle/ C port of the reference path on {self.threads} host threads: "
+                           f"tree+batches+lists {self.setup_s:.1f}s (serial, as in the "
+                           f"reference) and moments {self.moments_s:.1f}s measured in full; "
+                           f"evaluation of {len(self.sel)}/{self.batches.nb} random target "
+                           f"batches = {self.frac:.4f} of the pairs took {t:.1f}s; "
+                           f"extrapolated full step {est:.1f}s"),
+                "est_step_s": est}
+
+
+def cpu_baseline(system, cfg, econf, budget_pairs: float = 1.5e10):
+    return CpuReference(system, econf, budget_pairs).step()
 
 
 # ---------------------------------------------------------------------------
@@ -198,10 +213,11 @@ def run_reference(args, cfg):
         return
     econf = eval_config(cfg, args.batch_size, args.leaf_size)
     system = make_system(cfg)
+    ref = CpuReference(system, econf, budget_pairs=args.ref_budget)
     vals = []
     res = None
     for i in range(args.warmup + args.steps):
-        res = cpu_baseline(system, cfg, econf, budget_pairs=args.ref_budget)
+        res = ref.step()
         if i >= args.warmup:
             vals.append(res["value"])
         log(f"reference step {i}: {res['sample']}")

@@ -110,24 +110,17 @@ __device__ __forceinline__ void far_row(double (&acc)[kTpt], const double* qr,
 
 // ---------------------------------------------------------------------------
 // Far field.  M = n + 1 at compile time (k3 unrolled); M = 0: runtime degree.
-template <int KIND, int M, int kTpt, int MINB, int FORM>
-__global__ void __launch_bounds__(kWarps * 32, MINB)
-k_far_fast(EvalArgs a, const int2* __restrict__ items, int n_items, int* counter) {
-  extern __shared__ double smem[];
+// One work item: targets [t0, min(t0 + 32 kTpt, t1)) of batch b against the
+// batch's whole approximation list.
+template <int KIND, int M, int kTpt, int FORM>
+__device__ __forceinline__ void far_item(const EvalArgs& a, int b, int t0, int t1, double* pts,
+                                         double* qh, int lane) {
   const int m = M > 0 ? M : a.degree + 1;
   const int m3 = m * m * m;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int per_warp = 3 * kMaxM + 1 + a.mstride;   // +1 keeps qh 16-byte aligned
-  double* pts = smem + warp * per_warp;   // [3][kMaxM]
-  double* qh = pts + 3 * kMaxM + 1;       // [mstride]
-  for (int item = next_item(counter); item < n_items; item = next_item(counter)) {
-    const int2 it = items[item];
-    const int b = it.x;
-    const int t1 = a.bstop[b];
     double tx[kTpt], ty[kTpt], tz[kTpt], acc[kTpt];
 #pragma unroll
     for (int k = 0; k < kTpt; ++k) {
-      const int i = min(it.y + k * 32 + lane, t1 - 1);
+      const int i = min(t0 + k * 32 + lane, t1 - 1);
       tx[k] = a.tx[i];
       ty[k] = a.ty[i];
       tz[k] = a.tz[i];
@@ -213,9 +206,27 @@ k_far_fast(EvalArgs a, const int2* __restrict__ items, int n_items, int* counter
     }
 #pragma unroll
     for (int k = 0; k < kTpt; ++k) {
-      const int i = it.y + k * 32 + lane;
+      const int i = t0 + k * 32 + lane;
       if (i < t1) a.far_out[i] = acc[k];
     }
+}
+
+template <int KIND, int M, int kTpt, int MINB, int FORM>
+__global__ void __launch_bounds__(kWarps * 32, MINB)
+k_far_fast(EvalArgs a, const int2* __restrict__ items, int n_items, int* counter) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int per_warp = 3 * kMaxM + 1 + a.mstride;   // +1 keeps qh 16-byte aligned
+  double* pts = smem + warp * per_warp;   // [3][kMaxM]
+  double* qh = pts + 3 * kMaxM + 1;       // [mstride]
+  for (int item = next_item(counter); item < n_items; item = next_item(counter)) {
+    const int2 it = items[item];
+    const int t1 = a.bstop[it.x];
+    // a batch's last chunk with <= 32 targets runs one target per lane
+    if (kTpt > 1 && t1 - it.y <= 32)
+      far_item<KIND, M, 1, FORM>(a, it.x, it.y, t1, pts, qh, lane);
+    else
+      far_item<KIND, M, kTpt, FORM>(a, it.x, it.y, t1, pts, qh, lane);
   }
 }
 
@@ -235,20 +246,14 @@ __device__ __forceinline__ void stage_sources(double4* dst, const double4* src, 
   cp_async_commit();
 }
 
-template <int KIND, int kTpt, int MINB, int FORM>
-__global__ void __launch_bounds__(kWarps * 32, MINB)
-k_near_fast(EvalArgs a, const int2* __restrict__ items, int n_items, int* counter) {
-  __shared__ __align__(16) double4 stage[kWarps][2][kSrcChunk];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+template <int KIND, int kTpt, int FORM>
+__device__ __forceinline__ void near_item(const EvalArgs& a, int b, int t0, int t1,
+                                          double4 (*stage)[kSrcChunk], int lane) {
   const long long tb = __double_as_longlong(kSingularSq);   // d2 >= 0: bit order = value order
-  for (int item = next_item(counter); item < n_items; item = next_item(counter)) {
-    const int2 it = items[item];
-    const int b = it.x;
-    const int t1 = a.bstop[b];
     double tx[kTpt], ty[kTpt], tz[kTpt], acc[kTpt], comp[kTpt];
 #pragma unroll
     for (int k = 0; k < kTpt; ++k) {
-      const int i = min(it.y + k * 32 + lane, t1 - 1);
+      const int i = min(t0 + k * 32 + lane, t1 - 1);
       tx[k] = a.tx[i];
       ty[k] = a.ty[i];
       tz[k] = a.tz[i];
@@ -260,11 +265,11 @@ k_near_fast(EvalArgs a, const int2* __restrict__ items, int n_items, int* counte
       const EvalCluster c = a.clusters[a.d_idx[e]];
       const int nchunks = (c.stop - c.start + kSrcChunk - 1) / kSrcChunk;
       __syncwarp();
-      stage_sources(stage[warp][0], a.src4, c.start, c.stop, lane);
+      stage_sources(stage[0], a.src4, c.start, c.stop, lane);
       for (int ch = 0; ch < nchunks; ++ch) {
         const int buf = ch & 1;
         if (ch + 1 < nchunks) {
-          stage_sources(stage[warp][buf ^ 1], a.src4, c.start + (ch + 1) * kSrcChunk, c.stop,
+          stage_sources(stage[buf ^ 1], a.src4, c.start + (ch + 1) * kSrcChunk, c.stop,
                         lane);
           cp_async_wait<1>();
         } else {
@@ -277,7 +282,7 @@ k_near_fast(EvalArgs a, const int2* __restrict__ items, int n_items, int* counte
         for (int k = 0; k < kTpt; ++k) part[k] = 0.0;
 #pragma unroll 4
         for (int j = 0; j < jn; ++j) {
-          const double4 s = stage[warp][buf][j];
+          const double4 s = stage[buf][j];
 #pragma unroll
           for (int k = 0; k < kTpt; ++k) {
             const double dx = __dsub_rn(tx[k], s.x);
@@ -297,7 +302,7 @@ k_near_fast(EvalArgs a, const int2* __restrict__ items, int n_items, int* counte
     }
 #pragma unroll
     for (int k = 0; k < kTpt; ++k) {
-      const int i = it.y + k * 32 + lane;
+      const int i = t0 + k * 32 + lane;
       if (i < t1) {
         // approximations first, then the compensated direct sums on top
         // (engine.py:302-312, 335)
@@ -306,6 +311,20 @@ k_near_fast(EvalArgs a, const int2* __restrict__ items, int n_items, int* counte
         a.out[i] = __dadd_rn(total, cmp);
       }
     }
+}
+
+template <int KIND, int kTpt, int MINB, int FORM>
+__global__ void __launch_bounds__(kWarps * 32, MINB)
+k_near_fast(EvalArgs a, const int2* __restrict__ items, int n_items, int* counter) {
+  __shared__ __align__(16) double4 stage[kWarps][2][kSrcChunk];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int item = next_item(counter); item < n_items; item = next_item(counter)) {
+    const int2 it = items[item];
+    const int t1 = a.bstop[it.x];
+    if (kTpt > 1 && t1 - it.y <= 32)
+      near_item<KIND, 1, FORM>(a, it.x, it.y, t1, stage[warp], lane);
+    else
+      near_item<KIND, kTpt, FORM>(a, it.x, it.y, t1, stage[warp], lane);
   }
 }
 
