@@ -413,6 +413,8 @@ void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, 
   a.G = G;
   a.bstart = c->bstart.p;
   a.bstop = c->bstop.p;
+  a.bcenter = c->bcenter.p;
+  a.bradius = c->bradius.p;
   a.tx = T.x.p;
   a.ty = T.y.p;
   a.tz = T.z.p;

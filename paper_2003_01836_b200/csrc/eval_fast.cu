@@ -246,10 +246,50 @@ __device__ __forceinline__ void stage_sources(double4* dst, const double4* src, 
   cp_async_commit();
 }
 
+// Lower bound on the distance between the batch's bounding ball and a
+// cluster box (0 when they overlap).
+__device__ __forceinline__ double ball_box_gap(const double* bc, double br, const EvalCluster& c) {
+  double g2 = 0.0;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double lo = c.lo[d] - bc[d], hi = bc[d] - c.hi[d];
+    const double g = fmax(fmax(lo, hi), 0.0);
+    g2 = fma(g, g, g2);
+  }
+  return sqrt(g2) - br;
+}
+
+// One staged chunk of sources against kTpt targets.  MASKED applies the
+// reference's singular-pair exclusion (d^2 < 1e-28 skipped, engine.py:175)
+// on the integer pipe; the unmasked variant is used when no pair can be
+// singular.
+template <int KIND, int kTpt, int FORM, bool MASKED>
+__device__ __forceinline__ void near_chunk(double (&part)[kTpt], const double4* src, int jn,
+                                           const double (&tx)[kTpt], const double (&ty)[kTpt],
+                                           const double (&tz)[kTpt], double kappa) {
+  const long long tb = __double_as_longlong(kSingularSq);   // d2 >= 0: bit order = value order
+#pragma unroll 4
+  for (int j = 0; j < jn; ++j) {
+    const double4 s = src[j];
+#pragma unroll
+    for (int k = 0; k < kTpt; ++k) {
+      const double dx = __dsub_rn(tx[k], s.x);
+      const double dy = __dsub_rn(ty[k], s.y);
+      const double dz = __dsub_rn(tz[k], s.z);
+      const double d2 = fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx)));
+      if (MASKED) {
+        const bool ok = __double_as_longlong(d2) >= tb;
+        part[k] = pair_acc<KIND, FORM>(part[k], ok ? s.w : 0.0, ok ? d2 : 1.0, kappa);
+      } else {
+        part[k] = pair_acc<KIND, FORM>(part[k], s.w, d2, kappa);
+      }
+    }
+  }
+}
+
 template <int KIND, int kTpt, int FORM>
 __device__ __forceinline__ void near_item(const EvalArgs& a, int b, int t0, int t1,
                                           double4 (*stage)[kSrcChunk], int lane) {
-  const long long tb = __double_as_longlong(kSingularSq);   // d2 >= 0: bit order = value order
     double tx[kTpt], ty[kTpt], tz[kTpt], acc[kTpt], comp[kTpt];
 #pragma unroll
     for (int k = 0; k < kTpt; ++k) {
@@ -264,6 +304,12 @@ __device__ __forceinline__ void near_item(const EvalArgs& a, int b, int t0, int 
     for (int e = e0; e < e1; ++e) {
       const EvalCluster c = a.clusters[a.d_idx[e]];
       const int nchunks = (c.stop - c.start + kSrcChunk - 1) / kSrcChunk;
+      // The singular-pair test can only fire if the batch ball comes within
+      // ~1e-14 of the cluster box; otherwise the unmasked loop is exact.
+      const double* bc = a.bcenter + 3 * b;
+      const double scale =
+          fmax(fmax(fabs(bc[0]), fabs(bc[1])), fabs(bc[2])) + a.bradius[b];
+      const bool masked = ball_box_gap(bc, a.bradius[b], c) <= 1e-12 * (1.0 + scale);
       __syncwarp();
       stage_sources(stage[0], a.src4, c.start, c.stop, lane);
       for (int ch = 0; ch < nchunks; ++ch) {
@@ -280,21 +326,10 @@ __device__ __forceinline__ void near_item(const EvalArgs& a, int b, int t0, int 
         double part[kTpt];
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) part[k] = 0.0;
-#pragma unroll 4
-        for (int j = 0; j < jn; ++j) {
-          const double4 s = stage[buf][j];
-#pragma unroll
-          for (int k = 0; k < kTpt; ++k) {
-            const double dx = __dsub_rn(tx[k], s.x);
-            const double dy = __dsub_rn(ty[k], s.y);
-            const double dz = __dsub_rn(tz[k], s.z);
-            const double d2 = fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx)));
-            const bool ok = __double_as_longlong(d2) >= tb;
-            const double d2s = ok ? d2 : 1.0;
-            const double qs = ok ? s.w : 0.0;
-            part[k] = pair_acc<KIND, FORM>(part[k], qs, d2s, a.kappa);
-          }
-        }
+        if (masked)
+          near_chunk<KIND, kTpt, FORM, true>(part, stage[buf], jn, tx, ty, tz, a.kappa);
+        else
+          near_chunk<KIND, kTpt, FORM, false>(part, stage[buf], jn, tx, ty, tz, a.kappa);
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) neumaier(acc[k], comp[k], part[k]);
         __syncwarp();
