@@ -120,6 +120,7 @@ typedef struct {
   int64_t n_moments;
   int32_t degree;
   int32_t tree_depth, batch_depth;
+  int32_t n_groups;                /* source trees in the last evaluation (ranks) */
 } bltc_sizes;
 
 BLTC_API int bltc_get_sizes(bltc_ctx* ctx, bltc_sizes* out);
@@ -132,7 +133,8 @@ BLTC_API int bltc_export_tree(bltc_ctx* ctx, int which, int64_t* n_nodes_out, in
 /* Target batches in DFS (= ascending start) order. */
 BLTC_API int bltc_export_batches(bltc_ctx* ctx, int64_t* start, int64_t* stop, double* center,
                         double* radius);
-/* Interaction lists, CSR over batches: ptr sized n_batches+1. */
+/* Interaction lists, CSR over (batch, group) segments, batch-major: ptr sized
+ * n_batches*n_groups+1; entries are forest cluster ids. */
 BLTC_API int bltc_export_lists(bltc_ctx* ctx, int64_t* a_ptr, int64_t* a_idx, int64_t* d_ptr,
                       int64_t* d_idx);
 /* Moments: cluster ids [n_moments] and rows [n_moments][(n+1)^3]. */

@@ -49,7 +49,8 @@ class Sizes(ctypes.Structure):
                 ("n_clusters", ctypes.c_int64), ("n_batches", ctypes.c_int64),
                 ("n_approx", ctypes.c_int64), ("n_direct", ctypes.c_int64),
                 ("n_moments", ctypes.c_int64), ("degree", ctypes.c_int32),
-                ("tree_depth", ctypes.c_int32), ("batch_depth", ctypes.c_int32)]
+                ("tree_depth", ctypes.c_int32), ("batch_depth", ctypes.c_int32),
+                ("n_groups", ctypes.c_int32)]
 
 
 class PublishSizes(ctypes.Structure):

@@ -135,6 +135,70 @@ __global__ void k_unpermute(int64_t n, const double* sorted, const int32_t* perm
   if (i < n) phi[i] = sorted[perm[i]];
 }
 
+// Flattened TreeArray record of one cluster (decomp.py:137-189), as doubles
+// (all integers < 2^31 are exact): the unit the forest all-gather moves.
+constexpr int kRec = 18;
+enum RecField {
+  R_LO = 0, R_HI = 3, R_CENTER = 6, R_RADIUS = 9, R_COUNT = 10, R_CHILD_START = 11,
+  R_CHILD_COUNT = 12, R_ELIGIBLE = 13, R_START = 14, R_STOP = 15, R_MROW = 16
+};
+
+__global__ void k_pack_records(int64_t nn, const double* lo, const double* hi,
+                               const MacNode* mac, const EvalCluster* ecl, double* rec) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  double* r = rec + i * kRec;
+  const MacNode m = mac[i];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    r[R_LO + d] = lo[3 * i + d];
+    r[R_HI + d] = hi[3 * i + d];
+  }
+  r[R_CENTER] = m.cx;
+  r[R_CENTER + 1] = m.cy;
+  r[R_CENTER + 2] = m.cz;
+  r[R_RADIUS] = m.radius;
+  r[R_COUNT] = m.count;
+  r[R_CHILD_START] = m.child_start;
+  r[R_CHILD_COUNT] = m.child_count;
+  r[R_ELIGIBLE] = m.eligible;
+  r[R_START] = ecl[i].start;
+  r[R_STOP] = ecl[i].stop;
+  r[R_MROW] = ecl[i].mrow;
+  r[17] = 0.0;
+}
+
+// One owner's records -> the forest's MacNode / EvalCluster arrays, shifting
+// particle ranges and moment rows by the owner's offsets in the forest.
+__global__ void k_unpack_records(int64_t nn, const double* rec, int32_t p_off, int32_t row_off,
+                                 MacNode* mac, EvalCluster* ecl) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  const double* r = rec + i * kRec;
+  MacNode m;
+  m.cx = r[R_CENTER];
+  m.cy = r[R_CENTER + 1];
+  m.cz = r[R_CENTER + 2];
+  m.radius = r[R_RADIUS];
+  m.count = (int32_t)r[R_COUNT];
+  m.child_start = (int32_t)r[R_CHILD_START];
+  m.child_count = (int32_t)r[R_CHILD_COUNT];
+  m.eligible = (int32_t)r[R_ELIGIBLE];
+  mac[i] = m;
+  EvalCluster c;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    c.lo[d] = r[R_LO + d];
+    c.hi[d] = r[R_HI + d];
+  }
+  c.start = (int32_t)r[R_START] + p_off;
+  c.stop = (int32_t)r[R_STOP] + p_off;
+  const int32_t mrow = (int32_t)r[R_MROW];
+  c.mrow = mrow >= 0 ? mrow + row_off : -1;
+  c.pad = 0;
+  ecl[i] = c;
+}
+
 __global__ void k_widen(int64_t n, const int32_t* a, int64_t* out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) out[i] = a[i];
@@ -743,6 +807,7 @@ int bltc_get_sizes(bltc_ctx* c, bltc_sizes* out) {
     out->degree = c->params.degree;
     out->tree_depth = c->src.depth;
     out->batch_depth = c->tgt->depth;
+    out->n_groups = (int32_t)c->lists.n_groups;
   });
 }
 
@@ -810,25 +875,220 @@ int bltc_export_moments(bltc_ctx* c, int64_t* cluster_ids, double* rows) {
   });
 }
 
-int bltc_rank_build(bltc_ctx*, const bltc_params*, const double*, int64_t, const double*,
-                    const double*, const double*, const double*, int32_t) {
-  set_error("not implemented yet");
-  return BLTC_ERR_UNSUPPORTED;
+int bltc_rank_build(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64_t n,
+                    const double* x, const double* y, const double* z, const double* q,
+                    int32_t device_ptrs) {
+  return guarded([&] {
+    if (!c) throw UserError{BLTC_ERR_VALUE};
+    BLTC_CUDA(cudaSetDevice(c->device));
+    check_params(p);
+    if (n < 1) {
+      set_error("cannot partition an empty particle set");
+      throw UserError{BLTC_ERR_VALUE};
+    }
+    cudaStream_t st = c->st;
+    c->params = *p;
+    c->have_run = false;
+    c->rank_built = false;
+    const double* dx = x;
+    const double* dy = y;
+    const double* dz = z;
+    const double* dq = q;
+    if (!device_ptrs) {
+      const double* hs_[4] = {x, y, z, q};
+      for (int k = 0; k < 4; ++k) {
+        c->in[3 + k].resize(n);
+        BLTC_CUDA(cudaMemcpyAsync(c->in[3 + k].p, hs_[k], n * sizeof(double),
+                                  cudaMemcpyHostToDevice, st));
+      }
+      dx = c->in[3].p;
+      dy = c->in[4].p;
+      dz = c->in[5].p;
+      dq = c->in[6].p;
+    }
+    Timer tm(c->timing, st);
+    upload_nodes(c, p, cheb_s);
+    tm.mark();
+    // local tree + local batches (decomp.py:507-520)
+    build_partition(c->src, c->bs, n, dx, dy, dz, dq, p->leaf_size, st, c->hs);
+    if (p->batch_size == p->leaf_size) {
+      c->tgt = &c->src;
+    } else {
+      build_partition(c->tgt_own, c->bs, n, dx, dy, dz, nullptr, p->batch_size, st, c->hs);
+      c->tgt = &c->tgt_own;
+    }
+    build_batches(c, *c->tgt);
+    const int64_t nn = c->src.n_nodes;
+    c->mac.resize(nn);
+    c->ecl.resize(nn);
+    k_mac_nodes<<<grid_for(nn, 128), 128, 0, st>>>(nn, c->src.lo.p, c->src.hi.p, c->src.start.p,
+                                                   c->src.stop.p, c->src.child_start.p,
+                                                   c->src.child_count.p, c->mac.p);
+    BLTC_LAUNCH_CHECK();
+    k_eval_clusters<<<grid_for(nn, 128), 128, 0, st>>>(nn, c->src.lo.p, c->src.hi.p,
+                                                       c->src.start.p, c->src.stop.p, 0, c->ecl.p);
+    BLTC_LAUNCH_CHECK();
+    tm.mark();
+    // moments of every cluster another rank's MAC could accept (decomp.py:526-533;
+    // the reference publishes all eligible rows, only these can ever be read)
+    compute_moments(c, p, c->src, c->mac.p, c->ecl.p, 2, c->rows, 0);
+    tm.mark();
+    BLTC_CUDA(cudaStreamSynchronize(st));
+    c->rank_n = n;
+    c->rank_built = true;
+  });
 }
-int bltc_rank_publish_sizes(bltc_ctx*, bltc_publish_sizes*) {
-  set_error("not implemented yet");
-  return BLTC_ERR_UNSUPPORTED;
+
+int bltc_rank_publish_sizes(bltc_ctx* c, bltc_publish_sizes* out) {
+  return guarded([&] {
+    if (!c || !c->rank_built) {
+      set_error("bltc_rank_build has not run on this context");
+      throw UserError{BLTC_ERR_STATE};
+    }
+    out->n_clusters = c->src.n_nodes;
+    out->n_particles = c->rank_n;
+    out->n_moment_rows = c->n_moments;
+    out->record_doubles = kRec;
+  });
 }
-int bltc_rank_publish(bltc_ctx*, double*, double*, double*) {
-  set_error("not implemented yet");
-  return BLTC_ERR_UNSUPPORTED;
+
+int bltc_rank_publish(bltc_ctx* c, double* records, double* particles, double* moments) {
+  return guarded([&] {
+    if (!c || !c->rank_built) {
+      set_error("bltc_rank_build has not run on this context");
+      throw UserError{BLTC_ERR_STATE};
+    }
+    BLTC_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = c->st;
+    const int64_t nn = c->src.n_nodes, n = c->rank_n;
+    k_pack_records<<<grid_for(nn, 128), 128, 0, st>>>(nn, c->src.lo.p, c->src.hi.p, c->mac.p,
+                                                      c->ecl.p, records);
+    BLTC_LAUNCH_CHECK();
+    const double* src[4] = {c->src.x.p, c->src.y.p, c->src.z.p, c->src.q.p};
+    for (int k = 0; k < 4; ++k)
+      BLTC_CUDA(cudaMemcpyAsync(particles + k * n, src[k], n * sizeof(double),
+                                cudaMemcpyDeviceToDevice, st));
+    const int mstride = moment_stride(c->params.degree);
+    if (c->n_moments > 0)
+      BLTC_CUDA(cudaMemcpyAsync(moments, c->rows.p, c->n_moments * mstride * sizeof(double),
+                                cudaMemcpyDeviceToDevice, st));
+    BLTC_CUDA(cudaStreamSynchronize(st));
+  });
 }
-int bltc_rank_evaluate(bltc_ctx*, const bltc_params*, int32_t, int32_t, const int64_t*,
-                       const int64_t*, const int64_t*, const double* const*,
-                       const double* const*, const double* const*, double*, int32_t,
-                       bltc_stats*) {
-  set_error("not implemented yet");
-  return BLTC_ERR_UNSUPPORTED;
+
+int bltc_rank_evaluate(bltc_ctx* c, const bltc_params* p, int32_t ranks, int32_t my_rank,
+                       const int64_t* n_clusters, const int64_t* n_particles,
+                       const int64_t* n_moment_rows, const double* const* records,
+                       const double* const* particles, const double* const* moments,
+                       double* phi_out, int32_t device_ptrs, bltc_stats* stats) {
+  return guarded([&] {
+    if (!c || !c->rank_built) {
+      set_error("bltc_rank_build has not run on this context");
+      throw UserError{BLTC_ERR_STATE};
+    }
+    BLTC_CUDA(cudaSetDevice(c->device));
+    check_params(p);
+    if (ranks < 1 || my_rank < 0 || my_rank >= ranks) {
+      set_error("invalid ranks / my_rank");
+      throw UserError{BLTC_ERR_VALUE};
+    }
+    if (p->degree != c->params.degree || p->leaf_size != c->params.leaf_size ||
+        p->batch_size != c->params.batch_size) {
+      set_error("evaluation parameters differ from those of bltc_rank_build");
+      throw UserError{BLTC_ERR_VALUE};
+    }
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    cudaStream_t st = c->st;
+    const long long launches0 = g_launch_count;
+    Timer tm(c->timing, st);
+    tm.mark();
+    // owner order of _eval_rank (decomp.py:437-454): local first, then the
+    // remote owners ascending
+    std::vector<int> owners;
+    owners.push_back(my_rank);
+    for (int o = 0; o < ranks; ++o)
+      if (o != my_rank) owners.push_back(o);
+    const int G = ranks;
+    const int mstride = moment_stride(p->degree);
+    std::vector<int32_t> cl_off(G), p_off(G), row_off(G);
+    int64_t C = 0, P = 0, RW = 0;
+    for (int g = 0; g < G; ++g) {
+      const int o = owners[g];
+      cl_off[g] = (int32_t)C;
+      p_off[g] = (int32_t)P;
+      row_off[g] = (int32_t)RW;
+      C += n_clusters[o];
+      P += n_particles[o];
+      RW += n_moment_rows[o];
+    }
+    if (P > (int64_t)INT32_MAX / 2) {
+      set_error("forest above 2^30 particles per device");
+      throw UserError{BLTC_ERR_UNSUPPORTED};
+    }
+    c->f_mac.resize(C);
+    c->f_ecl.resize(C);
+    c->f_x.resize(P);
+    c->f_y.resize(P);
+    c->f_z.resize(P);
+    c->f_q.resize(P);
+    c->f_rows.resize(RW * mstride + 2);
+    std::vector<const MacNode*> trees(G);
+    for (int g = 0; g < G; ++g) {
+      const int o = owners[g];
+      const int64_t nc = n_clusters[o], np = n_particles[o];
+      k_unpack_records<<<grid_for(nc, 128), 128, 0, st>>>(nc, records[o], p_off[g], row_off[g],
+                                                          c->f_mac.p + cl_off[g],
+                                                          c->f_ecl.p + cl_off[g]);
+      BLTC_LAUNCH_CHECK();
+      double* dst[4] = {c->f_x.p, c->f_y.p, c->f_z.p, c->f_q.p};
+      for (int k = 0; k < 4; ++k)
+        BLTC_CUDA(cudaMemcpyAsync(dst[k] + p_off[g], particles[o] + k * np, np * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, st));
+      if (n_moment_rows[o] > 0)
+        BLTC_CUDA(cudaMemcpyAsync(c->f_rows.p + (size_t)row_off[g] * mstride, moments[o],
+                                  n_moment_rows[o] * mstride * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, st));
+      trees[g] = c->f_mac.p + cl_off[g];
+    }
+    c->params = *p;
+    build_lists(c, p, G, trees.data(), cl_off.data());
+    tm.mark();
+    if (p->mode == BLTC_MODE_FAST) {
+      c->f_src4.resize(P);
+      k_pack4<<<grid_for(P, 256), 256, 0, st>>>(P, c->f_x.p, c->f_y.p, c->f_z.p, c->f_q.p,
+                                                c->f_src4.p);
+      BLTC_LAUNCH_CHECK();
+    }
+    evaluate(c, p, G, c->f_ecl.p, c->f_x.p, c->f_y.p, c->f_z.p, c->f_q.p, c->f_src4.p,
+             c->f_rows.p, stats);
+    const int64_t n = c->rank_n;
+    c->phi_dev.resize(n);
+    k_unpermute<<<grid_for(n, 256), 256, 0, st>>>(n, c->out_sorted.p, c->tgt->perm.p,
+                                                  device_ptrs ? phi_out : c->phi_dev.p);
+    BLTC_LAUNCH_CHECK();
+    if (!device_ptrs)
+      BLTC_CUDA(cudaMemcpyAsync(phi_out, c->phi_dev.p, n * sizeof(double),
+                                cudaMemcpyDeviceToHost, st));
+    tm.mark();
+    unsigned long long* h = (unsigned long long*)c->hs.get(64);
+    BLTC_CUDA(cudaMemcpyAsync(h, c->lists.pairs.p, 2 * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, st));
+    BLTC_CUDA(cudaStreamSynchronize(st));
+    if (stats) {
+      stats->n_clusters = c->src.n_nodes;
+      stats->n_batches = c->bstart.n;
+      stats->direct_pairs = (int64_t)h[0];
+      stats->approx_pairs = (int64_t)h[1];
+      stats->setup_s = tm.secs(0, 1);
+      stats->compute_s = tm.secs(1, 2);
+      stats->total_s = tm.secs(0, 2);
+      stats->n_moments = c->n_moments;
+      stats->kernel_launches = g_launch_count - launches0;
+      stats->tree_depth = c->src.depth;
+      stats->batch_depth = c->tgt->depth;
+    }
+    c->have_run = true;
+  });
 }
 
 }  // extern "C"

@@ -1,0 +1,372 @@
+"""Multi-rank BLTC evaluation: one rank per GPU (decomp.py of the reference).
+
+``run_distributed(system, config, ranks, threads=1)`` keeps the reference's
+signature and results (decomp.py:483-593): targets are partitioned by
+recursive coordinate bisection (decomp.py:76-130, restated here on the host
+with the same numpy order statistics so every rank's particle order -- and
+therefore every bit of its tree -- matches the reference); each rank builds
+its own source tree, target batches and moments on its GPU; the forest is
+replicated by ONE all-gather of the published records (NCCL over NVLink when
+``torch.distributed`` runs one process per GPU); each rank then evaluates
+its batches against the local tree first and the remote trees in ascending
+owner order (decomp.py:437-454), exactly the reference's accumulation order.
+
+Replicating the whole forest replaces the reference's two-step one-sided LET
+fetch (decomp.py:354-399): every rank holds a superset of its locally
+essential tree, so the reference's sufficiency property holds trivially and
+the evaluation is unchanged.  A LET-minimal exchange is SURVEY.md 8(f) #2.
+
+Execution models:
+* ``torch.distributed`` initialised with world_size == ranks: this process is
+  one rank (its GPU = ``torch.cuda.current_device()``); the exchange is
+  ``all_gather`` over the process group (NCCL).
+* otherwise: the ranks run back to back in this process on one GPU and the
+  exchange is a no-op (the published device buffers are read in place).
+
+The per-rank device work goes through a rank engine; the product engine is
+:class:`DeviceRankEngine` (libbltc).  The host logic (partition, exchange,
+ordering, assembly) is engine-agnostic so it is unit-tested with world-size-2
+``gloo`` process groups on CPU.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .particles import Points
+from .tree_types import BoundingBox
+
+RECORD_DOUBLES = 18   # flattened TreeArray record (csrc/api.cu kRec)
+
+
+def moment_stride(degree: int) -> int:
+    m3 = (degree + 1) ** 3
+    return (m3 + 1) & ~1
+
+
+# ---------------------------------------------------------------------------
+# Recursive coordinate bisection (decomp.py:49-130)
+
+
+@dataclass(eq=False)
+class CutNode:
+    axis: int
+    value: float
+    left: "CutNode | int"
+    right: "CutNode | int"
+
+
+@dataclass(eq=False)
+class RcbPartition:
+    assignment: np.ndarray       # original index -> rank id
+    order: np.ndarray            # original indices grouped rank-contiguously
+    rank_start: np.ndarray       # length R+1 offsets into order
+    regions: list                # rank slabs tiling the root box
+    cuts: "CutNode | int"
+
+    def rank_indices(self, rank: int) -> np.ndarray:
+        return self.order[self.rank_start[rank]:self.rank_start[rank + 1]]
+
+    @property
+    def counts(self) -> np.ndarray:
+        return np.diff(self.rank_start)
+
+
+def _cut_axis(lo: np.ndarray, hi: np.ndarray) -> int:
+    return int(np.argmax(hi - lo))   # ties resolve to the lowest axis (decomp.py:71-73)
+
+
+def rcb_partition(points: Points, ranks: int) -> RcbPartition:
+    """Cut the longest extent of the current slab at an exact order statistic;
+    ranks split floor/ceil; per-rank counts differ by at most one."""
+    n = len(points)
+    if ranks < 1:
+        raise ValueError("ranks must be >= 1")
+    if n < ranks:
+        raise ValueError(f"need at least one particle per rank ({n} < {ranks})")
+    coords = (np.asarray(points.x), np.asarray(points.y), np.asarray(points.z))
+    root_lo = np.array([c.min() for c in coords])
+    root_hi = np.array([c.max() for c in coords])
+    order = np.arange(n)
+    assignment = np.empty(n, dtype=np.int64)
+    shares = np.array([(n * (r + 1)) // ranks - (n * r) // ranks for r in range(ranks)],
+                      dtype=np.int64)
+    regions: list = [None] * ranks
+
+    def recurse(start, stop, r0, r1, lo, hi):
+        if r1 - r0 == 1:
+            assignment[order[start:stop]] = r0
+            regions[r0] = BoundingBox(lo.copy(), hi.copy())
+            return r0
+        rm = r0 + (r1 - r0) // 2
+        n_left = int(shares[r0:rm].sum())
+        axis = _cut_axis(lo, hi)
+        idx = order[start:stop]
+        vals = coords[axis][idx]
+        if n_left > 0:
+            idx = idx[np.argpartition(vals, n_left - 1)]
+            order[start:stop] = idx
+        left_max = float(coords[axis][idx[:n_left]].max())
+        right_min = float(coords[axis][idx[n_left:]].min())
+        cut = 0.5 * (left_max + right_min)
+        lo_hi = hi.copy()
+        lo_hi[axis] = cut
+        hi_lo = lo.copy()
+        hi_lo[axis] = cut
+        left = recurse(start, start + n_left, r0, rm, lo, lo_hi)
+        right = recurse(start + n_left, stop, rm, r1, hi_lo, hi)
+        return CutNode(axis=axis, value=cut, left=left, right=right)
+
+    cuts = recurse(0, n, 0, ranks, root_lo, root_hi)
+    rank_start = np.concatenate(([0], np.cumsum(shares)))
+    return RcbPartition(assignment=assignment, order=order, rank_start=rank_start,
+                        regions=regions, cuts=cuts)
+
+
+# ---------------------------------------------------------------------------
+# Published rank data and its exchange
+
+
+@dataclass(eq=False)
+class Published:
+    """One rank's frozen data (RankWindows, decomp.py:197-208) as flat tensors:
+    records [n_clusters, 18], particles [4, n] (x, y, z, q reordered),
+    moments [n_rows, moment_stride]."""
+
+    records: object
+    particles: object
+    moments: object
+
+    @property
+    def sizes(self) -> tuple[int, int, int]:
+        return (int(self.records.shape[0]), int(self.particles.shape[1]),
+                int(self.moments.shape[0]))
+
+
+def all_gather_published(pub: Published, ranks: int, group=None) -> list[Published]:
+    """Replicate every rank's published data on every rank: one size
+    all-gather, then one padded all-gather per buffer (NCCL over NVLink for
+    CUDA tensors, gloo for CPU tensors)."""
+    import torch
+    import torch.distributed as dist
+
+    dev = pub.records.device
+    sizes = torch.tensor(pub.sizes, dtype=torch.int64, device=dev)
+    all_sizes = [torch.empty_like(sizes) for _ in range(ranks)]
+    dist.all_gather(all_sizes, sizes, group=group)
+    all_sizes = [tuple(int(v) for v in s.tolist()) for s in all_sizes]
+    ncols = pub.moments.shape[1]
+    out = []
+    flat = {}
+    for key, width, pos in (("records", RECORD_DOUBLES, 0), ("particles", 4, 1),
+                            ("moments", ncols, 2)):
+        counts = [s[pos] for s in all_sizes]
+        cap = max(1, max(counts)) * width
+        buf = torch.zeros(cap, dtype=torch.float64, device=dev)
+        mine = getattr(pub, key).reshape(-1)
+        buf[:mine.numel()] = mine
+        gathered = [torch.empty_like(buf) for _ in range(ranks)]
+        dist.all_gather(gathered, buf, group=group)
+        flat[key] = (gathered, counts)
+    for r in range(ranks):
+        nc, n, nrow = all_sizes[r]
+        rec = flat["records"][0][r][:nc * RECORD_DOUBLES].view(nc, RECORD_DOUBLES)
+        par = flat["particles"][0][r][:4 * n].view(4, n)
+        mom = flat["moments"][0][r][:nrow * ncols].view(nrow, ncols)
+        out.append(Published(rec, par, mom))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# The product rank engine: libbltc on one CUDA device
+
+
+class DeviceRankEngine:
+    """One rank's device pipeline (bltc_rank_build / _publish / _evaluate)."""
+
+    def __init__(self, config, mode: str | None = None, device: int | None = None,
+                 context=None):
+        import torch
+
+        from .engine import Context, make_params
+        self.torch = torch
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.ctx = context or Context(self.device)
+        self.params = make_params(config, mode, all_moments=False)
+        self.n = 0
+        self.stats = None
+
+    def build(self, x, y, z, q) -> None:
+        torch = self.torch
+        dev = torch.device("cuda", self.device)
+        self._inputs = [torch.as_tensor(np.ascontiguousarray(v, dtype=np.float64)
+                                        if not isinstance(v, torch.Tensor) else v,
+                                        device=dev).contiguous() for v in (x, y, z, q)]
+        self.n = int(self._inputs[0].shape[0])
+        self.ctx.rank_build(self.params, self.n, *[t.data_ptr() for t in self._inputs],
+                            device_ptrs=True)
+
+    def publish(self) -> Published:
+        torch = self.torch
+        sz = self.ctx.rank_publish_sizes()
+        dev = torch.device("cuda", self.device)
+        rec = torch.empty((sz["n_clusters"], RECORD_DOUBLES), dtype=torch.float64, device=dev)
+        par = torch.empty((4, sz["n_particles"]), dtype=torch.float64, device=dev)
+        mom = torch.empty((max(1, sz["n_moment_rows"]), moment_stride(self.params.degree)),
+                          dtype=torch.float64, device=dev)
+        self.ctx.rank_publish(rec.data_ptr(), par.data_ptr(), mom.data_ptr())
+        torch.cuda.synchronize(dev)
+        return Published(rec, par, mom[:sz["n_moment_rows"]])
+
+    def evaluate(self, ranks: int, my_rank: int, forest: list[Published]):
+        torch = self.torch
+        dev = torch.device("cuda", self.device)
+        phi = torch.empty(self.n, dtype=torch.float64, device=dev)
+        sizes = [p.sizes for p in forest]
+        # zero-row moment tensors still need a valid pointer
+        mom_ptrs = [p.moments.data_ptr() if p.moments.numel() else p.records.data_ptr()
+                    for p in forest]
+        self.stats = self.ctx.rank_evaluate(
+            self.params, ranks, my_rank, [s[0] for s in sizes], [s[1] for s in sizes],
+            [s[2] for s in sizes], [p.records.data_ptr() for p in forest],
+            [p.particles.data_ptr() for p in forest], mom_ptrs, phi.data_ptr(),
+            device_ptrs=True)
+        return phi
+
+
+# ---------------------------------------------------------------------------
+# Orchestration
+
+
+@dataclass(eq=False)
+class FetchStats:
+    """Per (origin, owner) exchange volume (decomp.py:324-331).  With the
+    replicated forest every origin receives the owner's whole tree."""
+
+    tree_records: int = 0
+    clusters: int = 0
+    moments: int = 0
+    particles: int = 0
+
+
+@dataclass(eq=False)
+class RankTimings:
+    rank: int
+    tree_s: float
+    moments_s: float
+    let_s: float
+    eval_s: float
+
+
+@dataclass(eq=False)
+class DistributedStats:
+    n_ranks: int
+    rank_counts: np.ndarray
+    n_clusters: int
+    n_batches: int
+    direct_pairs: int
+    approx_pairs: int
+    fetch_stats: dict = field(default_factory=dict)
+    rank_timings: list = field(default_factory=list)
+    setup_s: float = 0.0
+    precompute_s: float = 0.0
+    compute_s: float = 0.0
+    total_s: float = 0.0
+
+
+def _process_group_world(group):
+    try:
+        import torch.distributed as dist
+    except ImportError:
+        return None, 1, 0
+    if not (dist.is_available() and dist.is_initialized()):
+        return None, 1, 0
+    return dist, dist.get_world_size(group), dist.get_rank(group)
+
+
+def run_distributed(system, config, ranks: int, threads: int = 1, mode: str | None = None,
+                    group=None, engine_factory=None):
+    """decomp.py:483-593 on GPUs.  Returns (phi in original order, stats) on
+    every participating process.  ``threads`` is accepted and ignored."""
+    import time
+
+    import torch
+
+    del threads
+    if not system.coincident:
+        raise ValueError("distributed runs require targets and sources "
+                         "to be the same particle set")
+    t_start = time.perf_counter()
+    part = rcb_partition(system.sources, ranks)
+    dist, world, me = _process_group_world(group)
+    if world > 1 and world != ranks:
+        raise ValueError(f"ranks ({ranks}) must equal the process-group size ({world})")
+    mine = [me] if world > 1 else list(range(ranks))
+    factory = engine_factory or (lambda: DeviceRankEngine(config, mode))
+    engines = {r: factory() for r in mine}
+    src = system.sources
+    x, y, z = np.asarray(src.x), np.asarray(src.y), np.asarray(src.z)
+    q = np.asarray(system.charges)
+    timings = {}
+    t0 = time.perf_counter()
+    for r in mine:
+        idx = part.rank_indices(r)
+        tr = time.perf_counter()
+        engines[r].build(x[idx], y[idx], z[idx], q[idx])
+        timings[r] = [time.perf_counter() - tr, 0.0, 0.0, 0.0]
+    t_build = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    pubs = {r: engines[r].publish() for r in mine}
+    if world > 1:
+        forest = all_gather_published(pubs[me], ranks, group)
+    else:
+        forest = [pubs[r] for r in range(ranks)]
+    t_exchange = time.perf_counter() - t0
+    for r in mine:
+        timings[r][2] = t_exchange
+    t0 = time.perf_counter()
+    rank_phi = {}
+    for r in mine:
+        tr = time.perf_counter()
+        rank_phi[r] = engines[r].evaluate(ranks, r, forest)
+        timings[r][3] = time.perf_counter() - tr
+    t_eval = time.perf_counter() - t0
+
+    phi = np.empty(len(system.targets))
+    local = np.zeros(4, dtype=np.int64)   # direct, approx, clusters, batches
+    for r in mine:
+        st = engines[r].stats
+        local += [st.direct_pairs, st.approx_pairs, st.n_clusters, st.n_batches]
+    if world > 1:
+        dev = pubs[me].records.device
+        counts = part.counts
+        cap = int(counts.max())
+        buf = torch.zeros(cap, dtype=torch.float64, device=dev)
+        mine_phi = rank_phi[me].reshape(-1)
+        buf[:mine_phi.numel()] = mine_phi
+        gathered = [torch.empty_like(buf) for _ in range(ranks)]
+        dist.all_gather(gathered, buf, group=group)
+        for o in range(ranks):
+            phi[part.rank_indices(o)] = gathered[o][:counts[o]].cpu().numpy()
+        tot = torch.tensor(local, dtype=torch.int64, device=dev)
+        dist.all_reduce(tot, group=group)
+        local = tot.cpu().numpy()
+    else:
+        for o in range(ranks):
+            phi[part.rank_indices(o)] = rank_phi[o].detach().cpu().numpy()
+    fetch = {}
+    for r in mine:
+        for o in range(ranks):
+            if o != r:
+                nc, n, nrow = forest[o].sizes
+                fetch[(r, o)] = FetchStats(tree_records=nc, clusters=nc, moments=nrow,
+                                           particles=n)
+    total = time.perf_counter() - t_start
+    stats = DistributedStats(
+        n_ranks=ranks, rank_counts=part.counts, n_clusters=int(local[2]),
+        n_batches=int(local[3]), direct_pairs=int(local[0]), approx_pairs=int(local[1]),
+        fetch_stats=fetch,
+        rank_timings=[RankTimings(r, *timings[r]) for r in mine],
+        setup_s=t_build + t_exchange, precompute_s=0.0, compute_s=t_eval, total_s=total)
+    return phi, stats

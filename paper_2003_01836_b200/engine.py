@@ -172,6 +172,51 @@ class Context:
             sx, sy, sz, q, 1 if coincident else 0, phi_ptr, ctypes.byref(st)))
         return RunStats.from_c(st)
 
+    # -- distributed rank entry points (decomp.py:483-593) -----------------------
+    def rank_build(self, params: _lib.Params, n: int, x, y, z, q, device_ptrs: bool) -> None:
+        """Local tree, batches and moments of one rank.  x, y, z, q: numpy arrays
+        (device_ptrs False) or raw device pointers (True)."""
+        nodes = cheb_nodes(params.degree)
+        if device_ptrs:
+            args = [ctypes.c_void_p(int(v)) for v in (x, y, z, q)]
+        else:
+            args = [_lib.f64p(_f64(v)) for v in (x, y, z, q)]
+            self._keep = (x, y, z, q)
+        _lib.check(self._lib.bltc_rank_build(self.handle, ctypes.byref(params),
+                                             _lib.f64p(nodes), int(n), *args,
+                                             1 if device_ptrs else 0))
+
+    def rank_publish_sizes(self) -> dict:
+        ps = _lib.PublishSizes()
+        _lib.check(self._lib.bltc_rank_publish_sizes(self.handle, ctypes.byref(ps)))
+        return {name: getattr(ps, name) for name, _ in _lib.PublishSizes._fields_}
+
+    def rank_publish(self, records_ptr: int, particles_ptr: int, moments_ptr: int) -> None:
+        _lib.check(self._lib.bltc_rank_publish(self.handle, ctypes.c_void_p(records_ptr),
+                                               ctypes.c_void_p(particles_ptr),
+                                               ctypes.c_void_p(moments_ptr)))
+
+    def rank_evaluate(self, params: _lib.Params, ranks: int, my_rank: int, n_clusters,
+                      n_particles, n_moment_rows, records, particles, moments, phi_out,
+                      device_ptrs: bool) -> RunStats:
+        """Evaluate this rank's batches against the gathered forest (device
+        pointers per owner rank, owner order 0..R-1)."""
+        R = int(ranks)
+        nc = np.ascontiguousarray(n_clusters, dtype=np.int64)
+        npart = np.ascontiguousarray(n_particles, dtype=np.int64)
+        nrow = np.ascontiguousarray(n_moment_rows, dtype=np.int64)
+        arr = ctypes.c_void_p * R
+        rec = arr(*[ctypes.c_void_p(int(v)) for v in records])
+        par = arr(*[ctypes.c_void_p(int(v)) for v in particles])
+        mom = arr(*[ctypes.c_void_p(int(v)) for v in moments])
+        st = _lib.Stats()
+        out = ctypes.c_void_p(int(phi_out)) if device_ptrs else \
+            ctypes.c_void_p(phi_out.ctypes.data)
+        _lib.check(self._lib.bltc_rank_evaluate(
+            self.handle, ctypes.byref(params), R, int(my_rank), _lib.i64p(nc), _lib.i64p(npart),
+            _lib.i64p(nrow), rec, par, mom, out, 1 if device_ptrs else 0, ctypes.byref(st)))
+        return RunStats.from_c(st)
+
     # -- stage exports of the last run (bit-exact structure checks) ------------
     def sizes(self) -> _lib.Sizes:
         sz = _lib.Sizes()
@@ -208,8 +253,9 @@ class Context:
 
     def export_lists(self) -> dict:
         sz = self.sizes()
-        out = dict(a_ptr=np.empty(sz.n_batches + 1, np.int64), a_idx=np.empty(sz.n_approx, np.int64),
-                   d_ptr=np.empty(sz.n_batches + 1, np.int64), d_idx=np.empty(sz.n_direct, np.int64))
+        nseg = sz.n_batches * max(1, sz.n_groups)
+        out = dict(a_ptr=np.empty(nseg + 1, np.int64), a_idx=np.empty(sz.n_approx, np.int64),
+                   d_ptr=np.empty(nseg + 1, np.int64), d_idx=np.empty(sz.n_direct, np.int64))
         _lib.check(self._lib.bltc_export_lists(self.handle, _lib.i64p(out["a_ptr"]),
                                                _lib.i64p(out["a_idx"]), _lib.i64p(out["d_ptr"]),
                                                _lib.i64p(out["d_idx"])))

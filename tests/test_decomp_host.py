@@ -1,0 +1,124 @@
+"""Distributed host logic on CPU: RCB against the reference, and the full
+run_distributed orchestration (exchange, owner order, assembly) with
+world-size-2 gloo process groups and an oracle-backed rank engine."""
+import os
+import socket
+
+import numpy as np
+import pytest
+from conftest import golden, golden_system
+
+from paper_2003_01836_b200 import cli
+from paper_2003_01836_b200.decomp import rcb_partition
+from paper_2003_01836_b200.particles import Points
+
+
+@pytest.mark.parametrize("case", ["dist_r3", "dist_r4_yukawa"])
+def test_rcb_matches_reference_order(case):
+    g = golden(case)
+    s = golden_system(g)
+    part = rcb_partition(s.sources, int(g["ranks"]))
+    np.testing.assert_array_equal(part.order, g["order"])
+    np.testing.assert_array_equal(part.rank_start, g["rank_start"])
+
+
+def test_rcb_reference_cases():
+    # test_decomp.py:27-103 of the reference
+    corners = np.array([[sx, sy, sz] for sx in (-0.5, 0.5) for sy in (-0.5, 0.5)
+                        for sz in (-0.5, 0.5)])
+    part = rcb_partition(Points.from_array(corners), 2)
+    np.testing.assert_array_equal(part.counts, [4, 4])
+    for r in (0, 1):
+        assert len(set(corners[part.rank_indices(r), 0])) == 1
+    rng = np.random.default_rng(57)
+    part = rcb_partition(Points.from_array(rng.uniform(-1, 1, (100_000, 3))), 6)
+    assert set(part.counts.tolist()) == {16666, 16667}
+    rng = np.random.default_rng(59)
+    for n, ranks in ((1003, 7), (97, 13), (64, 64), (100, 3)):
+        part = rcb_partition(Points.from_array(rng.uniform(-1, 1, (n, 3))), ranks)
+        assert part.counts.sum() == n and part.counts.max() - part.counts.min() <= 1
+        assert np.array_equal(np.sort(part.order), np.arange(n))
+    with pytest.raises(ValueError):
+        rcb_partition(Points.from_array(rng.uniform(-1, 1, (3, 3))), 4)
+    with pytest.raises(ValueError):
+        rcb_partition(Points.from_array(rng.uniform(-1, 1, (3, 3))), 0)
+
+
+def test_run_distributed_requires_coincident():
+    import paper_2003_01836_b200 as bltc
+    from paper_2003_01836_b200.decomp import run_distributed
+    rng = np.random.default_rng(97)
+    t = Points.from_array(rng.uniform(-1, 1, (100, 3)))
+    s = Points.from_array(rng.uniform(-1, 1, (100, 3)))
+    system = bltc.ParticleSystem(targets=t, sources=s, charges=rng.uniform(-1, 1, 100))
+    with pytest.raises(ValueError):
+        run_distributed(system, bltc.EvalConfig(theta=0.7, degree=3), ranks=2)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, case, out_dir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+
+    import paper_2003_01836_b200 as bltc
+    from conftest import golden, golden_system
+    from paper_2003_01836_b200.decomp import run_distributed
+    from rank_engine_oracle import OracleRankEngine
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = golden(case)
+    s = golden_system(g)
+    kernel = [bltc.coulomb(), bltc.yukawa(float(g["kappa"]))][int(g["kind"])]
+    cfg = bltc.EvalConfig(theta=float(g["theta"]), degree=int(g["degree"]),
+                          leaf_size=int(g["leaf"]), batch_size=int(g["batch"]), kernel=kernel)
+    phi, st = run_distributed(s, cfg, ranks=world, engine_factory=lambda: OracleRankEngine(cfg))
+    np.save(os.path.join(out_dir, f"phi{rank}.npy"), phi)
+    np.save(os.path.join(out_dir, f"pairs{rank}.npy"), np.array([st.direct_pairs,
+                                                                 st.approx_pairs]))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_orchestration_matches_oracle(tmp_path, oracle):
+    """Two processes, gloo all-gather of the published buffers: the assembled
+    potentials equal the reference's run_distributed bitwise."""
+    import torch.multiprocessing as mp
+    case = "dist_r3"
+    g = golden(case)
+    s = golden_system(g)
+    src = s.sources
+    ref, info = oracle.run_distributed(src.x, src.y, src.z, s.charges, 2, float(g["theta"]),
+                                       int(g["degree"]), int(g["leaf"]), int(g["batch"]),
+                                       int(g["kind"]), float(g["kappa"]))
+    mp.start_processes(_worker, args=(2, _free_port(), case, str(tmp_path)), nprocs=2,
+                       join=True, start_method="spawn")
+    for r in range(2):
+        np.testing.assert_array_equal(np.load(tmp_path / f"phi{r}.npy"), ref)
+        pairs = np.load(tmp_path / f"pairs{r}.npy")
+        assert (int(pairs[0]), int(pairs[1])) == (info["direct_pairs"], info["approx_pairs"])
+
+
+def test_single_process_orchestration_matches_oracle(oracle):
+    """ranks=4 simulated in one process (the no-process-group path)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import paper_2003_01836_b200 as bltc
+    from paper_2003_01836_b200.decomp import run_distributed
+    from rank_engine_oracle import OracleRankEngine
+    g = golden("dist_r4_yukawa")
+    s = golden_system(g)
+    cfg = bltc.EvalConfig(theta=0.7, degree=6, leaf_size=300, batch_size=300,
+                          kernel=bltc.yukawa(0.5))
+    phi, st = run_distributed(s, cfg, ranks=4, engine_factory=lambda: OracleRankEngine(cfg))
+    np.testing.assert_array_equal(phi, g["phi"])
+    assert st.direct_pairs == int(g["direct_pairs"])
+    assert st.approx_pairs == int(g["approx_pairs"])
+    assert sorted(st.rank_counts.tolist()) == [2000] * 4
+    assert set(st.fetch_stats) == {(o, w) for o in range(4) for w in range(4) if o != w}

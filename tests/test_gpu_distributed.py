@@ -1,0 +1,72 @@
+"""GPU distributed path (bltc_rank_build / _publish / _evaluate through the
+DeviceRankEngine) with the ranks simulated back to back on one device: the
+semantics a one-process-per-GPU NCCL run computes, checked against the
+reference's run_distributed (golden vectors) and the oracle."""
+import os
+
+import numpy as np
+import pytest
+from conftest import golden, golden_system
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def bltc():
+    import paper_2003_01836_b200 as pkg
+    pkg._lib.load()
+    return pkg
+
+
+def _cfg(bltc, g):
+    kernel = [bltc.coulomb(), bltc.yukawa(float(g["kappa"]))][int(g["kind"])]
+    return bltc.EvalConfig(theta=float(g["theta"]), degree=int(g["degree"]),
+                           leaf_size=int(g["leaf"]), batch_size=int(g["batch"]), kernel=kernel)
+
+
+def _check(phi, ref, exact_bits, scale_tol=1e-13):
+    if exact_bits:
+        np.testing.assert_array_equal(phi, ref)
+    else:
+        assert np.abs(phi - ref).max() <= scale_tol * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("case", ["dist_r3", "dist_r4_yukawa"])
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+def test_simulated_ranks_match_reference(bltc, case, mode):
+    from paper_2003_01836_b200.decomp import run_distributed
+    g = golden(case)
+    s = golden_system(g)
+    phi, st = run_distributed(s, _cfg(bltc, g), ranks=int(g["ranks"]), mode=mode)
+    exact = mode == "parity" and int(g["kind"]) == 0
+    _check(phi, g["phi"], exact, 1e-14 if mode == "parity" else 1e-13)
+    assert st.direct_pairs == int(g["direct_pairs"])
+    assert st.approx_pairs == int(g["approx_pairs"])
+
+
+def test_single_rank_is_serial_engine_bitwise(bltc):
+    """R=1 reproduces treecode_potentials bitwise (test_decomp.py:214-221)."""
+    from paper_2003_01836_b200 import cli
+    from paper_2003_01836_b200.decomp import run_distributed
+    s = cli.generate_particles(5000, 91)
+    cfg = bltc.EvalConfig(theta=0.7, degree=5, leaf_size=250, batch_size=250)
+    serial, _ = bltc.treecode_potentials(s, cfg, mode="parity")
+    phi, st = run_distributed(s, cfg, ranks=1, mode="parity")
+    np.testing.assert_array_equal(phi, serial)
+    assert st.n_ranks == 1 and st.fetch_stats == {}
+
+
+@pytest.mark.parametrize("ranks", [2, 4, 8])
+def test_plummer_ranks_vs_oracle(bltc, oracle, ranks):
+    from paper_2003_01836_b200 import cli
+    from paper_2003_01836_b200.decomp import run_distributed
+    s = cli.generate_plummer(120_000, 5)
+    src = s.sources
+    cfg = bltc.EvalConfig(theta=0.8, degree=8, leaf_size=1000, batch_size=500)
+    ref, info = oracle.run_distributed(src.x, src.y, src.z, s.charges, ranks, 0.8, 8, 1000, 500,
+                                       0, 0.0, threads=os.cpu_count() or 1)
+    phi, st = run_distributed(s, cfg, ranks=ranks, mode="parity")
+    np.testing.assert_array_equal(phi, ref)
+    assert (st.direct_pairs, st.approx_pairs) == (info["direct_pairs"], info["approx_pairs"])
+    phi_f, _ = run_distributed(s, cfg, ranks=ranks, mode="fast")
+    _check(phi_f, ref, False)
