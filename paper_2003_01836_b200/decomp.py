@@ -370,3 +370,34 @@ def run_distributed(system, config, ranks: int, threads: int = 1, mode: str | No
         rank_timings=[RankTimings(r, *timings[r]) for r in mine],
         setup_s=t_build + t_exchange, precompute_s=0.0, compute_s=t_eval, total_s=total)
     return phi, stats
+
+
+class DeviceRankRunner:
+    """One rank of a one-process-per-GPU run with device-resident inputs:
+    the RCB partition is computed once (the paper also partitions outside the
+    timed region); each ``step()`` is a full distributed
+    evaluation -- local tree / batches / moments, the forest all-gather over
+    NCCL, evaluation of the local batches -- and returns the rank's stats."""
+
+    def __init__(self, ctx, system, config, mode: str | None = None, group=None):
+        import torch
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.ranks = dist.get_world_size(group)
+        self.me = dist.get_rank(group)
+        part = rcb_partition(system.sources, self.ranks)
+        idx = part.rank_indices(self.me)
+        src = system.sources
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.inputs = [torch.from_numpy(np.ascontiguousarray(np.asarray(a)[idx])).to(dev)
+                       for a in (src.x, src.y, src.z, system.charges)]
+        self.engine = DeviceRankEngine(config, mode, context=ctx)
+        self.n_local = int(idx.shape[0])
+        self.phi = None
+
+    def step(self):
+        self.engine.build(*self.inputs)
+        pub = self.engine.publish()
+        forest = all_gather_published(pub, self.ranks, self.group)
+        self.phi = self.engine.evaluate(self.ranks, self.me, forest)
+        return self.engine.stats
