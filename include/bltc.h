@@ -171,6 +171,17 @@ BLTC_API int bltc_rank_evaluate(bltc_ctx* ctx, const bltc_params* p, int32_t ran
                        const double* const* particles, const double* const* moments,
                        double* phi_out, int32_t device_ptrs, bltc_stats* stats);
 
+/* ---- Verification oracle on the device (cli.py:73-149) --
+ * Brute-force Neumaier direct sums at the targets idx[0..n_idx) (indices into
+ * tx/ty/tz; NULL idx = all n_t targets) over all sources, singular pairs
+ * skipped.  mode PARITY: sequential IEEE per target (bitwise the CPU oracle
+ * for Coulomb); FAST: split sources, rsqrt.  Host pointers. */
+BLTC_API int bltc_direct_sum(bltc_ctx* ctx, int32_t kernel_code, double kappa, int32_t mode,
+                             int64_t n_idx, const int64_t* idx, int64_t n_t, const double* tx,
+                             const double* ty, const double* tz, int64_t n_s, const double* sx,
+                             const double* sy, const double* sz, const double* q,
+                             double* out);
+
 /* ---- Diagnostics --------------------------------------------------------
  * Sustained FP64 FMA throughput of the device (DFMA/s), measured for about
  * `seconds`: the denominator of the FP64 roofline fraction bench.py reports. */

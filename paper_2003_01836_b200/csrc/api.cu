@@ -233,6 +233,9 @@ struct bltc_ctx {
   DBuf<int32_t> item_cnt, item_off, counters;
   DBuf<int2> items, items2;
   DBuf<double> partial;
+  DBuf<double2> dpartial;
+  DBuf<int64_t> didx;
+  DBuf<double> dout;
   DBuf<int32_t> flag;
   DBuf<int64_t> widen;
   bltc_params params{};
@@ -712,7 +715,8 @@ int bltc_destroy(bltc_ctx* c) {
     c->rows.release(); c->s_nodes.release(); c->w_nodes.release(); c->out_sorted.release();
     c->far_out.release(); c->phi_dev.release(); c->src4.release(); c->flag.release();
     c->widen.release(); c->item_cnt.release(); c->item_off.release(); c->counters.release();
-    c->items.release(); c->items2.release(); c->partial.release(); c->f_ecl.release(); c->f_mac.release(); c->f_x.release();
+    c->items.release(); c->items2.release(); c->partial.release(); c->dpartial.release();
+    c->didx.release(); c->dout.release(); c->f_ecl.release(); c->f_mac.release(); c->f_x.release();
     c->f_y.release(); c->f_z.release(); c->f_q.release(); c->f_rows.release();
     c->f_src4.release();
     c->hs.release();
@@ -872,6 +876,46 @@ int bltc_export_moments(bltc_ctx* c, int64_t* cluster_ids, double* rows) {
                                   m3 * sizeof(double), c->n_moments, cudaMemcpyDeviceToHost,
                                   c->st));
     BLTC_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
+int bltc_direct_sum(bltc_ctx* c, int32_t kernel_code, double kappa, int32_t mode,
+                    int64_t n_idx, const int64_t* idx, int64_t n_t, const double* tx,
+                    const double* ty, const double* tz, int64_t n_s, const double* sx,
+                    const double* sy, const double* sz, const double* q, double* out) {
+  return guarded([&] {
+    if (!c) throw UserError{BLTC_ERR_VALUE};
+    if (kernel_code < 0 || kernel_code > 2 || !std::isfinite(kappa) || kappa < 0.0 ||
+        n_t < 1 || n_s < 1 || n_idx < 0) {
+      set_error("invalid direct-sum arguments");
+      throw UserError{BLTC_ERR_VALUE};
+    }
+    BLTC_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = c->st;
+    const double* hs_[7] = {tx, ty, tz, sx, sy, sz, q};
+    const int64_t ns_[7] = {n_t, n_t, n_t, n_s, n_s, n_s, n_s};
+    for (int k = 0; k < 7; ++k) {
+      c->in[k].resize(ns_[k]);
+      BLTC_CUDA(cudaMemcpyAsync(c->in[k].p, hs_[k], ns_[k] * sizeof(double),
+                                cudaMemcpyHostToDevice, st));
+    }
+    const int64_t m = idx ? n_idx : n_t;
+    c->didx.resize(m);
+    if (idx) {
+      BLTC_CUDA(cudaMemcpyAsync(c->didx.p, idx, m * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    } else {
+      std::vector<int64_t> all(m);
+      for (int64_t i = 0; i < m; ++i) all[i] = i;
+      BLTC_CUDA(cudaMemcpyAsync(c->didx.p, all.data(), m * sizeof(int64_t),
+                                cudaMemcpyHostToDevice, st));
+      BLTC_CUDA(cudaStreamSynchronize(st));
+    }
+    c->dout.resize(m);
+    direct_sum_device(kernel_code, kappa, mode, m, c->didx.p, c->in[0].p, c->in[1].p,
+                      c->in[2].p, n_s, c->in[3].p, c->in[4].p, c->in[5].p, c->in[6].p,
+                      c->dout.p, c->src4, c->dpartial, st);
+    BLTC_CUDA(cudaMemcpyAsync(out, c->dout.p, m * sizeof(double), cudaMemcpyDeviceToHost, st));
+    BLTC_CUDA(cudaStreamSynchronize(st));
   });
 }
 

@@ -172,6 +172,22 @@ class Context:
             sx, sy, sz, q, 1 if coincident else 0, phi_ptr, ctypes.byref(st)))
         return RunStats.from_c(st)
 
+    def direct_sum(self, system, kernel, sample=None, mode: str = "parity") -> np.ndarray:
+        """Brute-force potentials at ``sample`` (all targets if None) on the
+        device -- the reference harness's verification oracle (cli.py:130-149)."""
+        t, s = system.targets, system.sources
+        tx, ty, tz = _f64(t.x), _f64(t.y), _f64(t.z)
+        sx, sy, sz, q = _f64(s.x), _f64(s.y), _f64(s.z), _f64(system.charges)
+        idx = None if sample is None else np.ascontiguousarray(sample, dtype=np.int64)
+        m = tx.shape[0] if idx is None else idx.shape[0]
+        out = np.empty(m)
+        _lib.check(self._lib.bltc_direct_sum(
+            self.handle, int(kernel.code), float(kernel.kappa), _MODES[mode], m,
+            None if idx is None else _lib.i64p(idx), tx.shape[0], _lib.f64p(tx), _lib.f64p(ty),
+            _lib.f64p(tz), sx.shape[0], _lib.f64p(sx), _lib.f64p(sy), _lib.f64p(sz),
+            _lib.f64p(q), _lib.f64p(out)))
+        return out
+
     # -- distributed rank entry points (decomp.py:483-593) -----------------------
     def rank_build(self, params: _lib.Params, n: int, x, y, z, q, device_ptrs: bool) -> None:
         """Local tree, batches and moments of one rank.  x, y, z, q: numpy arrays
