@@ -204,6 +204,45 @@ def cpu_baseline(system, cfg, econf, budget_pairs: float = 1.5e10):
 # ---------------------------------------------------------------------------
 
 
+def accuracy_block(ctx, system, econf, mode, phi, args) -> dict:
+    """Accuracy of the timed result at the full workload size.
+
+    * relative L2 error against a direct sum on the reference harness's
+      verification sample (cli.py:287-290: child-2 stream, M targets), for
+      the measured mode and for PARITY mode (which is the reference's own
+      result bit for bit -- tests/test_gpu_parity.py), so the two errors can
+      be compared (BASELINE.json: within 1%);
+    * per-target deviation of the measured mode from PARITY over ALL targets:
+      strict max |d_i| / |phi_i| and condition-aware max |d_i| / max |phi|;
+    * the GPU direct sum is cross-checked bitwise against the CPU oracle on a
+      few of the sample targets."""
+    from oracle import oracle as orc
+    from paper_2003_01836_b200 import cli
+    n = system.n_targets
+    sample = cli.sample_indices(n, args.accuracy_sample, seed=1)
+    t0 = time.perf_counter()
+    ds = ctx.direct_sum(system, econf.kernel, sample, mode="parity")
+    t_ds = time.perf_counter() - t0
+    s = system.sources
+    k = min(32, sample.shape[0])
+    cpu = orc.direct_sum(s.x, s.y, s.z, s.x, s.y, s.z, system.charges, econf.kernel.code,
+                         econf.kernel.kappa, sample[:k], threads=os.cpu_count() or 1)
+    phi_p, _ = ctx.treecode(system, econf, mode="parity")
+    err = cli.relative_error(ds, phi[sample])
+    err_p = cli.relative_error(ds, phi_p[sample])
+    d = np.abs(phi - phi_p)
+    nz = phi_p != 0
+    strict = float((d[nz] / np.abs(phi_p[nz])).max()) if nz.any() else 0.0
+    return {"sample": int(sample.shape[0]), "error": err, "error_parity_mode": err_p,
+            "error_ratio": err / err_p if err_p else None,
+            "vs_parity_strict_max_rel": strict,
+            "vs_parity_condition_aware": float(d.max() / np.abs(phi_p).max()),
+            "vs_parity_frac_targets_above_1e-10": float((d[nz] / np.abs(phi_p[nz]) > 1e-10).mean()),
+            "direct_sum": f"GPU bltc_direct_sum PARITY ({t_ds:.1f}s); bitwise equal to the CPU "
+                          f"oracle on {k} targets: {bool(np.array_equal(cpu, ds[:k]))}",
+            "parity_mode_is_reference": "PARITY == reference bitwise (tests/test_gpu_parity.py)"}
+
+
 def run_reference(args, cfg):
     """--impl reference: the reference's CPU algorithm (oracle port; the
     Python/numba reference itself is not installable on the box) on this
@@ -401,6 +440,11 @@ def run_ours(args, cfg):
     }
     if e2e is not None:
         line["e2e"] = e2e
+    if dist is None and not args.no_accuracy:
+        try:
+            line["accuracy"] = accuracy_block(ctx, system, econf, mode, out, args)
+        except Exception as exc:   # reported, never required for the timing line
+            line["accuracy"] = {"error": repr(exc)}
     if world == 1 and not args.no_cpu_baseline:
         try:
             cb = cpu_baseline(system, cfg, econf, budget_pairs=args.ref_budget)
@@ -428,6 +472,8 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=1.5e10,
                     help="pairs evaluated by the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-accuracy", action="store_true")
+    ap.add_argument("--accuracy-sample", type=int, default=4000)
     ap.add_argument("--rank-path", action="store_true",
                     help="use the distributed (RCB + NCCL all-gather) path even at N=1")
     args = ap.parse_args()
