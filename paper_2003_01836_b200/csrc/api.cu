@@ -232,6 +232,9 @@ struct bltc_ctx {
   DBuf<double4> src4;
   DBuf<int32_t> item_cnt, item_off, counters;
   DBuf<int2> items, items2;
+  DBuf<int32_t> pk_pc, pk_poff, pk_wcnt, pk_woff;   // packed FAST items
+  DBuf<int4> pk_items;
+  DBuf<uint8_t> pk_dmask;
   DBuf<double> partial;
   DBuf<double2> dpartial;
   DBuf<int64_t> didx;
@@ -508,6 +511,19 @@ void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, 
     c->far_out.resize(T.n);
     a.far_out = c->far_out.p;
     float far_ms = 0, near_ms = 0;
+    c->counters.resize(2);
+    if (packed_supported(p->kernel_code, p->degree)) {
+      PackedItems pi;
+      build_packed_items(a, c->pk_pc, c->pk_poff, c->pk_wcnt, c->pk_woff, c->pk_items,
+                         c->pk_dmask, c->lists.n_direct, c->bs.scan_tmp, c->hs, st, &pi);
+      launch_eval_packed(a, p->kernel_code, pi, c->counters.p, st, &far_ms, &near_ms,
+                         c->timing);
+      if (stats) {
+        stats->far_s = far_ms * 1e-3;
+        stats->near_s = near_ms * 1e-3;
+      }
+      return;
+    }
     const FastTuning tune = fast_tuning();
     const bool tuned = p->kernel_code == 0;
     const int far_chunk = 32 * (tuned && p->degree == 8 ? tune.far_tpt : 2);
@@ -715,7 +731,9 @@ int bltc_destroy(bltc_ctx* c) {
     c->rows.release(); c->s_nodes.release(); c->w_nodes.release(); c->out_sorted.release();
     c->far_out.release(); c->phi_dev.release(); c->src4.release(); c->flag.release();
     c->widen.release(); c->item_cnt.release(); c->item_off.release(); c->counters.release();
-    c->items.release(); c->items2.release(); c->partial.release(); c->dpartial.release();
+    c->items.release(); c->items2.release();
+    c->pk_pc.release(); c->pk_poff.release(); c->pk_wcnt.release(); c->pk_woff.release();
+    c->pk_items.release(); c->pk_dmask.release(); c->partial.release(); c->dpartial.release();
     c->didx.release(); c->dout.release(); c->f_ecl.release(); c->f_mac.release(); c->f_x.release();
     c->f_y.release(); c->f_z.release(); c->f_q.release(); c->f_rows.release();
     c->f_src4.release();

@@ -87,12 +87,18 @@ struct DBuf {
     reserve(count);
     n = count;
   }
+  // Grow to hold at least `count` elements, keeping the first min(n, cap).
+  // Each buffer checks its own capacity: buffers shared between partitions
+  // (BuildScratch) must not rely on another buffer's capacity as a proxy.
   void grow_keep(size_t count, cudaStream_t s) {
     if (count <= cap) return;
     T* q = nullptr;
     size_t c = count + count / 2;
+    if (c < 2 * cap) c = 2 * cap;
     BLTC_CUDA(cudaMalloc(&q, c * sizeof(T)));
-    if (p && n) BLTC_CUDA(cudaMemcpyAsync(q, p, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    const size_t keep = n < cap ? n : cap;
+    if (p && keep)
+      BLTC_CUDA(cudaMemcpyAsync(q, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
     if (p) {
       BLTC_CUDA(cudaStreamSynchronize(s));
       BLTC_CUDA(cudaFree(p));

@@ -1,0 +1,621 @@
+// FAST-mode evaluation with packed work items (the default FAST path).
+//
+// Target batches are octree leaves with at most N_B targets but usually far
+// fewer (C4, N_B = 500: median 105).  Splitting each batch into 64-target
+// chunks leaves lanes idle on every ragged tail (~10% of the lanes at
+// N_B = 500, ~18% at N_B = 250).  Here the batches' targets, each batch
+// padded to an even count, form one stream of target slots; a work item is
+// a 64-slot window of that stream (two targets per lane) and may span up to
+// kGMax consecutive batches ("segments").  Each lane walks its own batch's
+// interaction list; in step e every segment processes entry e of its own
+// list, so lanes stay converged, and a lane whose list has ended simply
+// discards its per-cluster partial.  Consecutive batches are octree
+// neighbours with similar lists, so little work is lost to ragged list
+// lengths (C4: 98.6% of the far-field lane work is useful at N_B = 500,
+// 97.6% at N_B = 250, against 90.5% / 81.8% for per-batch chunks).
+//
+//   far field  (_approx_tile, engine.py:216-252): per segment, the
+//     cluster's proxy points and its moment row (k1 slabs of (n+1)^2
+//     values, double-buffered with cp.async) are staged in the warp's shared
+//     memory; every lane reads its own segment's copy (broadcast loads).
+//   near field (_direct_tile, engine.py:151-213): per segment, the sources of
+//     its direct list form one stream (cluster after cluster, list order),
+//     staged kNearCh packed (x, y, z, q) records at a time (double-
+//     buffered); exhausted streams are padded with zero-charge records far
+//     away, which add exactly 0.
+// The per-pair arithmetic is eval_fast.cu's (rsqrt seed + cubic correction,
+// 7 / 12 FP64 slots per far / near pair).
+#include "bltc_internal.cuh"
+#include "eval_common.cuh"
+
+#include <cstdlib>
+
+namespace bltc {
+
+namespace {
+constexpr int kWarps = 8;     // warps per CTA
+constexpr int kGMax = 4;      // batches (segments) per work item
+constexpr int kSlots = 64;    // target slots per item: 2 per lane
+constexpr int kNearCh = 32;   // near field: sources per staged chunk and segment
+
+__device__ __forceinline__ double rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double xy = __dmul_rn(x, y);
+  const double e = fma(-xy, y, 1.0);
+  const double c = fma(0.375, e, 0.5);
+  const double ye = __dmul_rn(y, e);
+  return fma(ye, c, y);
+}
+
+// q / sqrt(d2) accumulated into acc (eval_fast.cu: one 3-register DFMA).
+__device__ __forceinline__ double coulomb_acc(double acc, double q, double d2) {
+  double y0;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(d2));
+  const double e = fma(-__dmul_rn(d2, y0), y0, 1.0);
+  const double c = fma(0.375, e, 0.5);
+  const double p = fma(e, c, 1.0);
+  const double qy = __dmul_rn(q, y0);
+  return fma(qy, p, acc);
+}
+
+template <int KIND>
+__device__ __forceinline__ double pair_acc(double acc, double q, double d2, double kappa) {
+  if (KIND == 0) return coulomb_acc(acc, q, d2);
+  const double y = rsqrt_fast(d2);
+  const double r = __dmul_rn(d2, y);
+  return fma(__dmul_rn(q, exp(-kappa * r)), y, acc);
+}
+
+__device__ __forceinline__ void neumaier(double& acc, double& comp, double t) {
+  const double s = __dadd_rn(acc, t);
+  const bool big = fabs(acc) >= fabs(t);
+  const double hi = big ? acc : t, lo = big ? t : acc;
+  comp = __dadd_rn(comp, __dadd_rn(__dsub_rn(hi, s), lo));
+  acc = s;
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ int next_item(int* counter) {
+  int it = 0;
+  if ((threadIdx.x & 31) == 0) it = atomicAdd(counter, 1);
+  return __shfl_sync(0xffffffffu, it, 0);
+}
+
+// First index j in [0, n] with a[j] > v (a non-decreasing).
+__device__ __forceinline__ int64_t upper_bound(const int32_t* a, int64_t n, int64_t v) {
+  int64_t lo = 0, hi = n + 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] > v) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
+// ---------------------------------------------------------------------------
+// Work items.  pc[b] = batch size rounded up to even; poff = exclusive scan
+// (slot offset of each batch, poff[nb] = total slots S).  Window w covers
+// slots [64 w, min(64 w + 64, S)); a window overlapping more than kGMax
+// batches is split into several items.  Item = {slot_begin, slot_end,
+// first batch, segments}.
+__global__ void k_pad_counts(int64_t nb, const int32_t* bstart, const int32_t* bstop,
+                             int32_t* pc) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b < nb) {
+    const int n = bstop[b] - bstart[b];
+    pc[b] = n + (n & 1);
+  } else if (b == nb) {
+    pc[b] = 0;
+  }
+}
+
+__device__ __forceinline__ void window_batches(int64_t nb, const int32_t* poff, int64_t w,
+                                               int64_t* s0, int64_t* s1, int64_t* bf,
+                                               int64_t* bl) {
+  const int64_t S = poff[nb];
+  *s0 = w * kSlots;
+  *s1 = min(*s0 + kSlots, S);
+  *bf = upper_bound(poff, nb, *s0) - 1;
+  *bl = upper_bound(poff, nb, *s1 - 1) - 1;
+}
+
+__global__ void k_window_counts(int64_t nb, const int32_t* poff, int64_t nw, int32_t* cnt) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w < nw) {
+    int64_t s0, s1, bf, bl;
+    window_batches(nb, poff, w, &s0, &s1, &bf, &bl);
+    cnt[w] = (int32_t)((bl - bf + kGMax) / kGMax);
+  } else if (w == nw) {
+    cnt[w] = 0;
+  }
+}
+
+__global__ void k_window_fill(int64_t nb, const int32_t* poff, int64_t nw, const int32_t* ioff,
+                              int4* items) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w >= nw) return;
+  int64_t s0, s1, bf, bl;
+  window_batches(nb, poff, w, &s0, &s1, &bf, &bl);
+  int32_t o = ioff[w];
+  for (int64_t ba = bf; ba <= bl; ba += kGMax) {
+    const int64_t be = min(ba + kGMax, bl + 1);   // exclusive
+    const int64_t sb = max(s0, (int64_t)poff[ba]);
+    const int64_t se = min(s1, (int64_t)poff[be]);
+    items[o++] = make_int4((int)sb, (int)se, (int)ba, (int)(be - ba));
+  }
+}
+
+// Per direct-list entry: can a pair of (batch, cluster) be singular?  The
+// singular-pair test (d^2 < 1e-28, engine.py:175) can only fire if the
+// batch ball comes within ~1e-14 of the cluster box.
+__global__ void k_direct_mask(int64_t nb, int G, const int32_t* d_ptr, const int32_t* d_idx,
+                              const EvalCluster* clusters, const double* bcenter,
+                              const double* bradius, uint8_t* mask) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const double* bc = bcenter + 3 * b;
+  const double br = bradius[b];
+  const double scale = fmax(fmax(fabs(bc[0]), fabs(bc[1])), fabs(bc[2])) + br;
+  for (int e = d_ptr[b * G]; e < d_ptr[(b + 1) * G]; ++e) {
+    const EvalCluster& c = clusters[d_idx[e]];
+    double g2 = 0.0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double lo = c.lo[d] - bc[d], hi = bc[d] - c.hi[d];
+      const double g = fmax(fmax(lo, hi), 0.0);
+      g2 = fma(g, g, g2);
+    }
+    mask[e] = (sqrt(g2) - br) <= 1e-12 * (1.0 + scale) ? 1 : 0;
+  }
+}
+
+// Lane layout of one item: slots slot_begin + 2 lane, +1.
+struct LaneTargets {
+  int g;          // segment of this lane
+  int i0, i1;     // target indices (i1 == i0 when the second slot is padding)
+  bool v0, v1;    // slot holds a real target
+};
+
+__device__ __forceinline__ LaneTargets lane_targets(const int4 it, const EvalArgs& a,
+                                                    const int32_t* poff, int lane) {
+  LaneTargets L;
+  int s = it.x + 2 * lane;
+  const bool on = s < it.y;
+  if (!on) s = it.x;
+  L.g = 0;
+#pragma unroll
+  for (int k = 1; k < kGMax; ++k)
+    if (k < it.w && s >= poff[it.z + k]) L.g = k;
+  const int b = it.z + L.g;
+  L.i0 = a.bstart[b] + (s - poff[b]);
+  const int stop = a.bstop[b];
+  L.v0 = on;
+  L.v1 = on && (L.i0 + 1 < stop);
+  L.i1 = L.v1 ? L.i0 + 1 : L.i0;
+  return L;
+}
+
+// ---------------------------------------------------------------------------
+// Far field.  Shared memory per warp and segment: proxy points [3][M] and
+// two k1 slabs of M*M moments; segment regions are offset by one double so
+// that lanes of different segments read different banks.
+template <int M>
+struct FarSmem {
+  static constexpr int kPts = 3 * M;
+  static constexpr int kSlab = M * M;
+  static constexpr int kSeg = kPts + 2 * kSlab + 1;          // doubles per segment
+  static constexpr int kWarp = kGMax * kSeg + 1;             // doubles per warp
+};
+
+template <int KIND, int M>
+__device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it,
+                                                const int32_t* poff, double* wsm, int lane) {
+  using SM = FarSmem<M>;
+  const LaneTargets L = lane_targets(it, a, poff, lane);
+  const double tx[2] = {a.tx[L.i0], a.tx[L.i1]};
+  const double ty[2] = {a.ty[L.i0], a.ty[L.i1]};
+  const double tz[2] = {a.tz[L.i0], a.tz[L.i1]};
+  double acc[2] = {0.0, 0.0};
+
+  // segment lists (warp-uniform)
+  int e0[kGMax], len[kGMax];
+  int maxlen = 0, mylen = 0;
+#pragma unroll
+  for (int k = 0; k < kGMax; ++k) {
+    e0[k] = 0;
+    len[k] = 0;
+    if (k < it.w) {
+      const int64_t b = it.z + k;
+      e0[k] = a.a_ptr[b * a.G];
+      len[k] = a.a_ptr[(b + 1) * a.G] - e0[k];
+    }
+    maxlen = max(maxlen, len[k]);
+    if (k == L.g) mylen = len[k];
+  }
+  double* my = wsm + L.g * SM::kSeg;    // this lane's segment region
+  const double* mpts = my;
+  const double* mslab = my + SM::kPts;
+
+  const double* rows[kGMax];
+  for (int e = 0; e < maxlen; ++e) {
+    __syncwarp();
+    // stage proxy points and slab 0 of every live segment
+#pragma unroll
+    for (int k = 0; k < kGMax; ++k) {
+      rows[k] = nullptr;
+      if (e < len[k]) {
+        const EvalCluster* c = a.clusters + a.a_idx[e0[k] + e];
+        rows[k] = a.moments + (size_t)c->mrow * a.mstride;
+        double* seg = wsm + k * SM::kSeg;
+        for (int i = lane; i < SM::kPts; i += 32) {
+          const int d = i / M, kk = i - d * M;
+          seg[i] = cheb_point_dev(a.degree, kk, c->lo[d], c->hi[d], a.s_nodes);
+        }
+        double* slab = seg + SM::kPts;
+        for (int i = lane; i < SM::kSlab; i += 32) cp_async8(slab + i, rows[k] + i);
+      }
+    }
+    cp_async_commit();
+    const bool act = e < mylen;
+    double part[2] = {0.0, 0.0};
+    __syncwarp();   // proxy points (plain stores) visible to the warp
+    double dz2[2][M];
+#pragma unroll
+    for (int k3 = 0; k3 < M; ++k3) {
+      const double p3 = mpts[2 * M + k3];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const double dz = __dsub_rn(tz[t], p3);
+        dz2[t][k3] = __dmul_rn(dz, dz);
+      }
+    }
+    for (int k1 = 0; k1 < M; ++k1) {
+      if (k1 + 1 < M) {
+#pragma unroll
+        for (int k = 0; k < kGMax; ++k) {
+          if (rows[k] != nullptr) {
+            double* slab = wsm + k * SM::kSeg + SM::kPts + ((k1 + 1) & 1) * SM::kSlab;
+            const double* src = rows[k] + (size_t)(k1 + 1) * SM::kSlab;
+            for (int i = lane; i < SM::kSlab; i += 32) cp_async8(slab + i, src + i);
+          }
+        }
+        cp_async_commit();
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+      const double p1 = mpts[k1];
+      double dx2[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const double dx = __dsub_rn(tx[t], p1);
+        dx2[t] = __dmul_rn(dx, dx);
+      }
+      const double* qr = mslab + (k1 & 1) * SM::kSlab;
+#pragma unroll 1
+      for (int k2 = 0; k2 < M; ++k2, qr += M) {
+        const double p2 = mpts[M + k2];
+        double dxy2[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const double dy = __dsub_rn(ty[t], p2);
+          dxy2[t] = fma(dy, dy, dx2[t]);
+        }
+#pragma unroll
+        for (int k3 = 0; k3 < M; ++k3) {
+          const double qv = qr[k3];
+#pragma unroll
+          for (int t = 0; t < 2; ++t)
+            part[t] = pair_acc<KIND>(part[t], qv, __dadd_rn(dxy2[t], dz2[t][k3]), a.kappa);
+        }
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t) acc[t] = __dadd_rn(acc[t], act ? part[t] : 0.0);
+  }
+  if (L.v0) a.far_out[L.i0] = acc[0];
+  if (L.v1) a.far_out[L.i1] = acc[1];
+}
+
+template <int KIND, int M, int MINB>
+__global__ void __launch_bounds__(kWarps * 32, MINB)
+k_far_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int32_t* poff,
+             int* counter) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* wsm = smem + warp * FarSmem<M>::kWarp;
+  for (int item = next_item(counter); item < n_items; item = next_item(counter))
+    far_packed_item<KIND, M>(a, items[item], poff, wsm, lane);
+}
+
+// ---------------------------------------------------------------------------
+// Near field.
+struct NearSmem {
+  // [segment][buffer][kNearCh] packed sources; +1 record between segments
+  static constexpr int kSeg = 2 * kNearCh + 1;
+  static constexpr int kWarp = kGMax * kSeg;
+};
+
+template <int KIND, bool MASKED>
+__device__ __forceinline__ void near_chunk(double (&part)[2], const double4* src,
+                                           const double (&tx)[2], const double (&ty)[2],
+                                           const double (&tz)[2], double kappa) {
+  const long long tb = __double_as_longlong(kSingularSq);   // d2 >= 0: bit order = value order
+#pragma unroll 4
+  for (int j = 0; j < kNearCh; ++j) {
+    const double4 s = src[j];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const double dx = __dsub_rn(tx[t], s.x);
+      const double dy = __dsub_rn(ty[t], s.y);
+      const double dz = __dsub_rn(tz[t], s.z);
+      const double d2 = fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx)));
+      if (MASKED) {
+        const bool ok = __double_as_longlong(d2) >= tb;
+        part[t] = pair_acc<KIND>(part[t], ok ? s.w : 0.0, ok ? d2 : 1.0, kappa);
+      } else {
+        part[t] = pair_acc<KIND>(part[t], s.w, d2, kappa);
+      }
+    }
+  }
+}
+
+// Stage the next kNearCh records of every live segment's source stream.
+// Stream position per segment: (list entry ce, offset co within its cluster);
+// lane `lane` stages record `lane` of each segment.  Returns whether any
+// staged record needs the singular-pair mask.
+__device__ __forceinline__ bool near_stage(const EvalArgs& a, const uint8_t* dmask,
+                                           const int (&e0)[kGMax], const int (&len)[kGMax],
+                                           int (&ce)[kGMax], int (&co)[kGMax], double4* wsm,
+                                           int buf, int lane) {
+  bool need_mask = false;
+#pragma unroll
+  for (int k = 0; k < kGMax; ++k) {
+    double4* dst = wsm + k * NearSmem::kSeg + buf * kNearCh + lane;
+    int e = ce[k], o = co[k] + lane;
+    int start = 0;
+    while (e < len[k]) {
+      const EvalCluster& c = a.clusters[a.d_idx[e0[k] + e]];
+      const int n = c.stop - c.start;
+      if (o < n) {
+        start = c.start;
+        break;
+      }
+      o -= n;
+      ++e;
+    }
+    if (e < len[k]) {
+      const double4* s = a.src4 + start + o;
+      cp_async16(dst, s);
+      cp_async16(reinterpret_cast<char*>(dst) + 16, reinterpret_cast<const char*>(s) + 16);
+      need_mask |= dmask[e0[k] + e] != 0;
+    } else {
+      *dst = make_double4(1e150, 1e150, 1e150, 0.0);   // contributes exactly 0
+    }
+    // new stream position: one past lane 31's record
+    const int ne = __shfl_sync(0xffffffffu, e, 31);
+    const int no = __shfl_sync(0xffffffffu, o, 31);
+    ce[k] = ne;
+    co[k] = ne < len[k] ? no + 1 : 0;
+  }
+  cp_async_commit();
+  return __any_sync(0xffffffffu, need_mask);
+}
+
+template <int KIND>
+__device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 it,
+                                                 const int32_t* poff, const uint8_t* dmask,
+                                                 double4* wsm, int lane) {
+  const LaneTargets L = lane_targets(it, a, poff, lane);
+  const double tx[2] = {a.tx[L.i0], a.tx[L.i1]};
+  const double ty[2] = {a.ty[L.i0], a.ty[L.i1]};
+  const double tz[2] = {a.tz[L.i0], a.tz[L.i1]};
+  double acc[2] = {0.0, 0.0}, comp[2] = {0.0, 0.0};
+
+  int e0[kGMax], len[kGMax], ce[kGMax], co[kGMax];
+#pragma unroll
+  for (int k = 0; k < kGMax; ++k) {
+    e0[k] = 0;
+    len[k] = 0;
+    if (k < it.w) {
+      const int64_t b = it.z + k;
+      e0[k] = a.d_ptr[b * a.G];
+      len[k] = a.d_ptr[(b + 1) * a.G] - e0[k];
+    }
+    ce[k] = 0;
+    co[k] = 0;
+  }
+  const double4* mine = wsm + L.g * NearSmem::kSeg;
+  bool live = false;
+#pragma unroll
+  for (int k = 0; k < kGMax; ++k) live |= ce[k] < len[k];
+  if (live) {
+    __syncwarp();
+    bool masked = near_stage(a, dmask, e0, len, ce, co, wsm, 0, lane);
+    for (int buf = 0;; buf ^= 1) {
+      bool more = false;
+#pragma unroll
+      for (int k = 0; k < kGMax; ++k) more |= ce[k] < len[k];
+      bool masked_next = false;
+      if (more) {
+        masked_next = near_stage(a, dmask, e0, len, ce, co, wsm, buf ^ 1, lane);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+      double part[2] = {0.0, 0.0};
+      if (masked)
+        near_chunk<KIND, true>(part, mine + buf * kNearCh, tx, ty, tz, a.kappa);
+      else
+        near_chunk<KIND, false>(part, mine + buf * kNearCh, tx, ty, tz, a.kappa);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) neumaier(acc[t], comp[t], part[t]);
+      __syncwarp();
+      if (!more) break;
+      masked = masked_next;
+    }
+  }
+  // approximations first, then the compensated direct sums on top
+  // (engine.py:302-312, 335)
+  if (L.v0) {
+    double total = acc[0], cmp = comp[0];
+    neumaier(total, cmp, a.far_out[L.i0]);
+    a.out[L.i0] = __dadd_rn(total, cmp);
+  }
+  if (L.v1) {
+    double total = acc[1], cmp = comp[1];
+    neumaier(total, cmp, a.far_out[L.i1]);
+    a.out[L.i1] = __dadd_rn(total, cmp);
+  }
+}
+
+template <int KIND, int MINB>
+__global__ void __launch_bounds__(kWarps * 32, MINB)
+k_near_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int32_t* poff,
+              const uint8_t* dmask, int* counter) {
+  extern __shared__ double4 nsmem[];
+  double4* smem = nsmem;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double4* wsm = smem + warp * NearSmem::kWarp;
+  for (int item = next_item(counter); item < n_items; item = next_item(counter))
+    near_packed_item<KIND>(a, items[item], poff, dmask, wsm, lane);
+}
+
+// ---------------------------------------------------------------------------
+template <typename K>
+int persistent_grid(K kernel, int threads, size_t smem) {
+  int dev = 0, sms = 0, per_sm = 0;
+  BLTC_CUDA(cudaGetDevice(&dev));
+  BLTC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  BLTC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+  return sms * (per_sm > 0 ? per_sm : 1);
+}
+
+template <int KIND, int M>
+void far_packed_launch(const EvalArgs& a, const PackedItems& it, int* counter, cudaStream_t st) {
+  const size_t smem = sizeof(double) * kWarps * FarSmem<M>::kWarp;
+  auto kern = k_far_packed<KIND, M, 2>;
+  BLTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = persistent_grid(kern, kWarps * 32, smem);
+  kern<<<grid, kWarps * 32, smem, st>>>(a, it.items, it.n_items, it.poff, counter);
+  BLTC_LAUNCH_CHECK();
+}
+
+template <int KIND>
+bool far_packed_dispatch(const EvalArgs& a, const PackedItems& it, int* counter,
+                         cudaStream_t st) {
+  switch (a.degree + 1) {
+    case 5: far_packed_launch<KIND, 5>(a, it, counter, st); return true;
+    case 6: far_packed_launch<KIND, 6>(a, it, counter, st); return true;
+    case 8: far_packed_launch<KIND, 8>(a, it, counter, st); return true;
+    case 9: far_packed_launch<KIND, 9>(a, it, counter, st); return true;
+    case 11: far_packed_launch<KIND, 11>(a, it, counter, st); return true;
+    default: return false;
+  }
+}
+
+template <int KIND>
+void near_packed_launch(const EvalArgs& a, const PackedItems& it, int* counter,
+                        cudaStream_t st) {
+  const size_t smem = sizeof(double4) * kWarps * NearSmem::kWarp;
+  auto kern = k_near_packed<KIND, 2>;
+  BLTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = persistent_grid(kern, kWarps * 32, smem);
+  kern<<<grid, kWarps * 32, smem, st>>>(a, it.items, it.n_items, it.poff, it.dmask, counter);
+  BLTC_LAUNCH_CHECK();
+}
+}  // namespace
+
+bool packed_supported(int kind, int degree) {
+  if (const char* e = std::getenv("BLTC_PACK"))
+    if (std::atoi(e) == 0) return false;
+  if (kind != 0 && kind != 1) return false;
+  const int m = degree + 1;
+  return m == 5 || m == 6 || m == 8 || m == 9 || m == 11;
+}
+
+void build_packed_items(const EvalArgs& a, DBuf<int32_t>& pc, DBuf<int32_t>& poff,
+                        DBuf<int32_t>& wcnt, DBuf<int32_t>& woff, DBuf<int4>& items,
+                        DBuf<uint8_t>& dmask, int64_t n_direct, DBuf<int32_t>& scan_tmp,
+                        HostScratch& hs, cudaStream_t st, PackedItems* out) {
+  const int64_t nb = a.nb;
+  pc.resize(nb + 1);
+  poff.resize(nb + 1);
+  k_pad_counts<<<(int)((nb + 1 + 255) / 256), 256, 0, st>>>(nb, a.bstart, a.bstop, pc.p);
+  BLTC_LAUNCH_CHECK();
+  exclusive_scan_i32(pc.p, poff.p, nb + 1, scan_tmp, st);
+  int32_t* h = (int32_t*)hs.get(64);
+  BLTC_CUDA(cudaMemcpyAsync(h, poff.p + nb, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  BLTC_CUDA(cudaStreamSynchronize(st));
+  const int64_t S = h[0];
+  const int64_t nw = (S + kSlots - 1) / kSlots;
+  wcnt.resize(nw + 1);
+  woff.resize(nw + 1);
+  k_window_counts<<<(int)((nw + 1 + 255) / 256), 256, 0, st>>>(nb, poff.p, nw, wcnt.p);
+  BLTC_LAUNCH_CHECK();
+  exclusive_scan_i32(wcnt.p, woff.p, nw + 1, scan_tmp, st);
+  BLTC_CUDA(cudaMemcpyAsync(h, woff.p + nw, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  BLTC_CUDA(cudaStreamSynchronize(st));
+  out->n_items = h[0];
+  items.resize(out->n_items + 1);
+  if (nw > 0) {
+    k_window_fill<<<(int)((nw + 255) / 256), 256, 0, st>>>(nb, poff.p, nw, woff.p, items.p);
+    BLTC_LAUNCH_CHECK();
+  }
+  dmask.resize(n_direct + 1);
+  if (nb > 0) {
+    k_direct_mask<<<(int)((nb + 127) / 128), 128, 0, st>>>(nb, a.G, a.d_ptr, a.d_idx,
+                                                            a.clusters, a.bcenter, a.bradius,
+                                                            dmask.p);
+    BLTC_LAUNCH_CHECK();
+  }
+  out->items = items.p;
+  out->poff = poff.p;
+  out->dmask = dmask.p;
+}
+
+void launch_eval_packed(const EvalArgs& a, int kind, const PackedItems& it, int* counters,
+                        cudaStream_t st, float* far_ms, float* near_ms, bool timing) {
+  if (a.nb == 0) return;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+  if (timing) {
+    BLTC_CUDA(cudaEventCreate(&e0));
+    BLTC_CUDA(cudaEventCreate(&e1));
+    BLTC_CUDA(cudaEventCreate(&e2));
+  }
+  BLTC_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int), st));
+  if (timing) BLTC_CUDA(cudaEventRecord(e0, st));
+  if (kind == 0) far_packed_dispatch<0>(a, it, counters, st);
+  else far_packed_dispatch<1>(a, it, counters, st);
+  if (timing) BLTC_CUDA(cudaEventRecord(e1, st));
+  if (kind == 0) near_packed_launch<0>(a, it, counters + 1, st);
+  else near_packed_launch<1>(a, it, counters + 1, st);
+  if (timing) {
+    BLTC_CUDA(cudaEventRecord(e2, st));
+    BLTC_CUDA(cudaEventSynchronize(e2));
+    BLTC_CUDA(cudaEventElapsedTime(far_ms, e0, e1));
+    BLTC_CUDA(cudaEventElapsedTime(near_ms, e1, e2));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+  }
+}
+
+}  // namespace bltc

@@ -443,8 +443,7 @@ void build_partition(Partition& P, BuildScratch& S, int64_t n, const double* dx,
   // node storage (grown as levels are added)
   int64_t cap = std::max<int64_t>(1024, 2 * n / std::max<int64_t>(1, max_count) + 64);
   auto ensure_nodes = [&](int64_t need) {
-    if (need <= (int64_t)P.start.cap) return;
-    int64_t c = std::max<int64_t>(need, 2 * (int64_t)P.start.cap);
+    const int64_t c = need;
     P.start.n = P.stop.n = P.child_start.n = P.child_count.n = P.level.n = P.n_nodes;
     P.lo.n = P.hi.n = P.n_nodes * 3;
     S.box_u.n = P.n_nodes * 6;

@@ -224,3 +224,30 @@ def test_oracle_parity_mid_size(bltc, ctx, oracle, gen, n, leaf, batch, deg, the
     np.testing.assert_array_equal(phi, ref)
     phi_f, _ = ctx.treecode(s, cfg, mode="fast")
     _phi_check(phi_f, ref, 0, exact=False)
+
+
+def test_context_reuse_across_sizes(bltc, oracle):
+    """One context serving runs whose node counts grow and shrink (the
+    partition scratch is shared between the source tree and the target
+    batches, and grown level by level): structures stay bit-exact."""
+    from paper_2003_01836_b200 import cli
+    s = cli.generate_plummer(120_000, 5)
+    src = s.sources
+    c = bltc.Context(0)
+    try:
+        for leaf, batch in [(2000, 2000), (400, 60), (2000, 25), (60, 400), (1000, 250)]:
+            cfg = bltc.EvalConfig(theta=0.8, degree=4, leaf_size=leaf, batch_size=batch)
+            c.treecode(s, cfg, mode="fast")
+            tree = oracle.build_source_tree(src.x, src.y, src.z, s.charges, leaf)
+            t = c.export_tree(0)
+            np.testing.assert_array_equal(t["perm"], tree.perm)
+            np.testing.assert_array_equal(t["start"], tree.start)
+            np.testing.assert_array_equal(t["lo"], tree.lo)
+            np.testing.assert_array_equal(t["hi"], tree.hi)
+            bt = oracle.build_target_batches(src.x, src.y, src.z, batch)
+            b = c.export_batches()
+            np.testing.assert_array_equal(b["start"], bt.start)
+            np.testing.assert_array_equal(b["stop"], bt.stop)
+            np.testing.assert_array_equal(b["radius"], bt.radius)
+    finally:
+        c.close()
