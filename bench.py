@@ -45,11 +45,12 @@ CONFIGS = {
                gen="uniform", n=1_000_000, kind=1, kappa=0.5, degree=8, theta=0.8, leaf=2000,
                batch=2000),
     # N_B (batch size) is the performance knob; the CPU
-    # baseline / reference arm run with the same value.  500 is the fastest
-    # measured for C4 on B200 (N_B=2000: 1.18 s, 1000: 1.10 s, 500: 1.07 s).
+    # baseline / reference arm run with the same value.  250 is the fastest
+    # measured for C4 on B200 with packed work items (N_B=125: 0.97 s,
+    # 250: 0.965 s, 500: 1.02 s, 1000: 1.11 s; tools/sweep_c4.py).
     "c4": dict(workload="C4: N=8M Plummer (a=1, r<=10a), Coulomb, n=8, theta=0.8",
                gen="plummer", n=8_000_000, kind=0, kappa=0.0, degree=8, theta=0.8, leaf=2000,
-               batch=500),
+               batch=250),
     "c4u": dict(workload="N=8M uniform cube, Coulomb, n=8, theta=0.8", gen="uniform",
                 n=8_000_000, kind=0, kappa=0.0, degree=8, theta=0.8, leaf=2000, batch=2000),
     "c5": dict(workload="C5: N=64M uniform cube, Coulomb, n=10, theta=0.7", gen="uniform",

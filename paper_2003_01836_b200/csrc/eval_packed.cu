@@ -36,7 +36,7 @@ namespace {
 constexpr int kWarps = 8;     // warps per CTA
 constexpr int kGMax = 4;      // batches (segments) per work item
 constexpr int kSlots = 64;    // target slots per item: 2 per lane
-constexpr int kNearCh = 32;   // near field: sources per staged chunk and segment
+constexpr int kNearCh = 32;   // near field default: sources per staged chunk and segment
 
 __device__ __forceinline__ double rsqrt_fast(double x) {
   double y;
@@ -210,66 +210,98 @@ __device__ __forceinline__ LaneTargets lane_targets(const int4 it, const EvalArg
 }
 
 // ---------------------------------------------------------------------------
-// Far field.  Shared memory per warp and segment: proxy points [3][M] and
-// two k1 slabs of M*M moments; segment regions are offset by one double so
-// that lanes of different segments read different banks.
+// Far field.  Shared memory per warp: a header with each segment's list
+// range and current moment row (kept out of registers: the pair loop needs
+// them for its ILP), then per segment the proxy points [3][M] and two k1
+// slabs of M*M moments; segment regions are offset by one double so that
+// lanes of different segments read different banks.
 template <int M>
 struct FarSmem {
+  static constexpr int kHdr = 2 * kGMax;                     // doubles
   static constexpr int kPts = 3 * M;
   static constexpr int kSlab = M * M;
   static constexpr int kSeg = kPts + 2 * kSlab + 1;          // doubles per segment
-  static constexpr int kWarp = kGMax * kSeg + 1;             // doubles per warp
+  static constexpr int kWarp = kHdr + kGMax * kSeg + 1;      // doubles per warp
 };
 
-template <int KIND, int M>
+struct FarHdr {
+  int e0[kGMax];
+  int len[kGMax];
+  const double* row[kGMax];   // current moment row (nullptr: segment idle)
+};
+static_assert(sizeof(FarHdr) <= 2 * kGMax * sizeof(double) + kGMax * sizeof(double),
+              "far header");
+
+template <int M>
+__device__ __forceinline__ void far_stage_slab(double* wsm, const FarHdr* H, int k1, int lane) {
+  using SM = FarSmem<M>;
+#pragma unroll
+  for (int k = 0; k < kGMax; ++k) {
+    const double* row = H->row[k];
+    if (row != nullptr) {
+      double* slab = wsm + SM::kHdr + k * SM::kSeg + SM::kPts + (k1 & 1) * SM::kSlab;
+      const double* src = row + (size_t)k1 * SM::kSlab;
+      for (int i = lane; i < SM::kSlab; i += 32) cp_async8(slab + i, src + i);
+    }
+  }
+  cp_async_commit();
+}
+
+template <int KIND, int M, int KU>
 __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it,
                                                 const int32_t* poff, double* wsm, int lane) {
   using SM = FarSmem<M>;
+  FarHdr* H = reinterpret_cast<FarHdr*>(wsm);
   const LaneTargets L = lane_targets(it, a, poff, lane);
   const double tx[2] = {a.tx[L.i0], a.tx[L.i1]};
   const double ty[2] = {a.ty[L.i0], a.ty[L.i1]};
   const double tz[2] = {a.tz[L.i0], a.tz[L.i1]};
   double acc[2] = {0.0, 0.0};
 
-  // segment lists (warp-uniform)
-  int e0[kGMax], len[kGMax];
+  // segment list ranges (warp-uniform) into the header
   int maxlen = 0, mylen = 0;
-#pragma unroll
-  for (int k = 0; k < kGMax; ++k) {
-    e0[k] = 0;
-    len[k] = 0;
-    if (k < it.w) {
-      const int64_t b = it.z + k;
-      e0[k] = a.a_ptr[b * a.G];
-      len[k] = a.a_ptr[(b + 1) * a.G] - e0[k];
+  __syncwarp();
+  if (lane < kGMax) {
+    int e0 = 0, len = 0;
+    if (lane < it.w) {
+      const int64_t b = it.z + lane;
+      e0 = a.a_ptr[b * a.G];
+      len = a.a_ptr[(b + 1) * a.G] - e0;
     }
-    maxlen = max(maxlen, len[k]);
-    if (k == L.g) mylen = len[k];
+    H->e0[lane] = e0;
+    H->len[lane] = len;
   }
-  double* my = wsm + L.g * SM::kSeg;    // this lane's segment region
-  const double* mpts = my;
-  const double* mslab = my + SM::kPts;
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < kGMax; ++k) maxlen = max(maxlen, H->len[k]);
+  mylen = H->len[L.g];
+  const double* mpts = wsm + SM::kHdr + L.g * SM::kSeg;   // this lane's segment region
+  const double* mslab = mpts + SM::kPts;
 
-  const double* rows[kGMax];
   for (int e = 0; e < maxlen; ++e) {
     __syncwarp();
-    // stage proxy points and slab 0 of every live segment
+    // this step's cluster of every segment: header row pointers, proxy points
+    if (lane < kGMax) {
+      const double* row = nullptr;
+      if (e < H->len[lane]) {
+        const EvalCluster* c = a.clusters + a.a_idx[H->e0[lane] + e];
+        row = a.moments + (size_t)c->mrow * a.mstride;
+      }
+      H->row[lane] = row;
+    }
+    __syncwarp();
 #pragma unroll
     for (int k = 0; k < kGMax; ++k) {
-      rows[k] = nullptr;
-      if (e < len[k]) {
-        const EvalCluster* c = a.clusters + a.a_idx[e0[k] + e];
-        rows[k] = a.moments + (size_t)c->mrow * a.mstride;
-        double* seg = wsm + k * SM::kSeg;
+      if (H->row[k] != nullptr) {
+        const EvalCluster* c = a.clusters + a.a_idx[H->e0[k] + e];
+        double* seg = wsm + SM::kHdr + k * SM::kSeg;
         for (int i = lane; i < SM::kPts; i += 32) {
           const int d = i / M, kk = i - d * M;
           seg[i] = cheb_point_dev(a.degree, kk, c->lo[d], c->hi[d], a.s_nodes);
         }
-        double* slab = seg + SM::kPts;
-        for (int i = lane; i < SM::kSlab; i += 32) cp_async8(slab + i, rows[k] + i);
       }
     }
-    cp_async_commit();
+    far_stage_slab<M>(wsm, H, 0, lane);
     const bool act = e < mylen;
     double part[2] = {0.0, 0.0};
     __syncwarp();   // proxy points (plain stores) visible to the warp
@@ -285,15 +317,7 @@ __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it
     }
     for (int k1 = 0; k1 < M; ++k1) {
       if (k1 + 1 < M) {
-#pragma unroll
-        for (int k = 0; k < kGMax; ++k) {
-          if (rows[k] != nullptr) {
-            double* slab = wsm + k * SM::kSeg + SM::kPts + ((k1 + 1) & 1) * SM::kSlab;
-            const double* src = rows[k] + (size_t)(k1 + 1) * SM::kSlab;
-            for (int i = lane; i < SM::kSlab; i += 32) cp_async8(slab + i, src + i);
-          }
-        }
-        cp_async_commit();
+        far_stage_slab<M>(wsm, H, k1 + 1, lane);
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
@@ -307,7 +331,7 @@ __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it
         dx2[t] = __dmul_rn(dx, dx);
       }
       const double* qr = mslab + (k1 & 1) * SM::kSlab;
-#pragma unroll 1
+#pragma unroll KU
       for (int k2 = 0; k2 < M; ++k2, qr += M) {
         const double p2 = mpts[M + k2];
         double dxy2[2];
@@ -333,7 +357,7 @@ __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it
   if (L.v1) a.far_out[L.i1] = acc[1];
 }
 
-template <int KIND, int M, int MINB>
+template <int KIND, int M, int MINB, int KU>
 __global__ void __launch_bounds__(kWarps * 32, MINB)
 k_far_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int32_t* poff,
              int* counter) {
@@ -341,24 +365,25 @@ k_far_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int3
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* wsm = smem + warp * FarSmem<M>::kWarp;
   for (int item = next_item(counter); item < n_items; item = next_item(counter))
-    far_packed_item<KIND, M>(a, items[item], poff, wsm, lane);
+    far_packed_item<KIND, M, KU>(a, items[item], poff, wsm, lane);
 }
 
 // ---------------------------------------------------------------------------
 // Near field.
+template <int CH>
 struct NearSmem {
-  // [segment][buffer][kNearCh] packed sources; +1 record between segments
-  static constexpr int kSeg = 2 * kNearCh + 1;
+  // [segment][buffer][CH] packed sources; +1 record between segments
+  static constexpr int kSeg = 2 * CH + 1;
   static constexpr int kWarp = kGMax * kSeg;
 };
 
-template <int KIND, bool MASKED>
+template <int KIND, int CH, bool MASKED>
 __device__ __forceinline__ void near_chunk(double (&part)[2], const double4* src,
                                            const double (&tx)[2], const double (&ty)[2],
                                            const double (&tz)[2], double kappa) {
   const long long tb = __double_as_longlong(kSingularSq);   // d2 >= 0: bit order = value order
 #pragma unroll 4
-  for (int j = 0; j < kNearCh; ++j) {
+  for (int j = 0; j < CH; ++j) {
     const double4 s = src[j];
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
@@ -376,49 +401,111 @@ __device__ __forceinline__ void near_chunk(double (&part)[2], const double4* src
   }
 }
 
-// Stage the next kNearCh records of every live segment's source stream.
-// Stream position per segment: (list entry ce, offset co within its cluster);
-// lane `lane` stages record `lane` of each segment.  Returns whether any
-// staged record needs the singular-pair mask.
+// One segment's source stream: the sources of its direct list, cluster
+// after cluster in list order.  Warp-uniform state: list entry e, offset o
+// within that cluster, the cluster's (start, count, mask flag) and the next
+// entry's, loaded one advance ahead so that staging a chunk needs no
+// dependent loads in the common case.
+struct Stream {
+  int e0, len;        // list segment [e0, e0 + len)
+  int e, o;           // position
+  int cs, cn, ns, nn; // current / next cluster: first source, count
+  bool cm, nm;        // current / next: singular pairs possible
+};
+
+__device__ __forceinline__ void stream_entry(const EvalArgs& a, const uint8_t* dmask, int ent,
+                                             int* start, int* count, bool* m) {
+  const EvalCluster& c = a.clusters[a.d_idx[ent]];
+  *start = c.start;
+  *count = c.stop - c.start;
+  *m = dmask[ent] != 0;
+}
+
+__device__ __forceinline__ void stream_init(const EvalArgs& a, const uint8_t* dmask, Stream& S,
+                                            int e0, int len) {
+  S.e0 = e0;
+  S.len = len;
+  S.e = 0;
+  S.o = 0;
+  S.cs = S.cn = S.ns = S.nn = 0;
+  S.cm = S.nm = false;
+  if (len > 0) stream_entry(a, dmask, e0, &S.cs, &S.cn, &S.cm);
+  if (len > 1) stream_entry(a, dmask, e0 + 1, &S.ns, &S.nn, &S.nm);
+}
+
+// Stage record o + r of the stream into dst[r]; returns whether it may form
+// singular pairs.
+__device__ __forceinline__ bool stream_stage(const EvalArgs& a, const uint8_t* dmask,
+                                             const Stream& S, double4* dst, int r0) {
+  bool need_mask = false;
+  int src = -1;
+  if (S.e < S.len) {
+    const int r = S.o + r0;
+    if (r < S.cn) {
+      src = S.cs + r;
+      need_mask = S.cm;
+    } else if (r - S.cn < S.nn) {
+      src = S.ns + (r - S.cn);
+      need_mask = S.nm;
+    } else {
+      // the chunk spans more than two clusters (small clusters): walk
+      int rr = r - S.cn - S.nn;
+      for (int e = S.e + 2; e < S.len; ++e) {
+        int st, n;
+        bool m;
+        stream_entry(a, dmask, S.e0 + e, &st, &n, &m);
+        if (rr < n) {
+          src = st + rr;
+          need_mask = m;
+          break;
+        }
+        rr -= n;
+      }
+    }
+  }
+  if (src >= 0) {
+    const double4* sp = a.src4 + src;
+    cp_async16(dst + r0, sp);
+    cp_async16(reinterpret_cast<char*>(dst + r0) + 16, reinterpret_cast<const char*>(sp) + 16);
+  } else {
+    dst[r0] = make_double4(1e150, 1e150, 1e150, 0.0);   // contributes exactly 0
+  }
+  return need_mask;
+}
+
+template <int CH>
+__device__ __forceinline__ void stream_advance(const EvalArgs& a, const uint8_t* dmask,
+                                               Stream& S) {
+  S.o += CH;
+  while (S.e < S.len && S.o >= S.cn) {
+    S.o -= S.cn;
+    ++S.e;
+    S.cs = S.ns;
+    S.cn = S.nn;
+    S.cm = S.nm;
+    S.nn = 0;
+    if (S.e + 1 < S.len) stream_entry(a, dmask, S.e0 + S.e + 1, &S.ns, &S.nn, &S.nm);
+  }
+}
+
+// Stage the next chunk of every live segment into buffer `buf`.
+template <int CH>
 __device__ __forceinline__ bool near_stage(const EvalArgs& a, const uint8_t* dmask,
-                                           const int (&e0)[kGMax], const int (&len)[kGMax],
-                                           int (&ce)[kGMax], int (&co)[kGMax], double4* wsm,
-                                           int buf, int lane) {
+                                           Stream (&S)[kGMax], double4* wsm, int buf,
+                                           int lane) {
   bool need_mask = false;
 #pragma unroll
   for (int k = 0; k < kGMax; ++k) {
-    double4* dst = wsm + k * NearSmem::kSeg + buf * kNearCh + lane;
-    int e = ce[k], o = co[k] + lane;
-    int start = 0;
-    while (e < len[k]) {
-      const EvalCluster& c = a.clusters[a.d_idx[e0[k] + e]];
-      const int n = c.stop - c.start;
-      if (o < n) {
-        start = c.start;
-        break;
-      }
-      o -= n;
-      ++e;
-    }
-    if (e < len[k]) {
-      const double4* s = a.src4 + start + o;
-      cp_async16(dst, s);
-      cp_async16(reinterpret_cast<char*>(dst) + 16, reinterpret_cast<const char*>(s) + 16);
-      need_mask |= dmask[e0[k] + e] != 0;
-    } else {
-      *dst = make_double4(1e150, 1e150, 1e150, 0.0);   // contributes exactly 0
-    }
-    // new stream position: one past lane 31's record
-    const int ne = __shfl_sync(0xffffffffu, e, 31);
-    const int no = __shfl_sync(0xffffffffu, o, 31);
-    ce[k] = ne;
-    co[k] = ne < len[k] ? no + 1 : 0;
+    double4* dst = wsm + k * NearSmem<CH>::kSeg + buf * CH;
+#pragma unroll
+    for (int r = 0; r < CH; r += 32) need_mask |= stream_stage(a, dmask, S[k], dst, r + lane);
+    stream_advance<CH>(a, dmask, S[k]);
   }
   cp_async_commit();
   return __any_sync(0xffffffffu, need_mask);
 }
 
-template <int KIND>
+template <int KIND, int CH>
 __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 it,
                                                  const int32_t* poff, const uint8_t* dmask,
                                                  double4* wsm, int lane) {
@@ -428,33 +515,31 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
   const double tz[2] = {a.tz[L.i0], a.tz[L.i1]};
   double acc[2] = {0.0, 0.0}, comp[2] = {0.0, 0.0};
 
-  int e0[kGMax], len[kGMax], ce[kGMax], co[kGMax];
+  Stream S[kGMax];
 #pragma unroll
   for (int k = 0; k < kGMax; ++k) {
-    e0[k] = 0;
-    len[k] = 0;
+    int e0 = 0, len = 0;
     if (k < it.w) {
       const int64_t b = it.z + k;
-      e0[k] = a.d_ptr[b * a.G];
-      len[k] = a.d_ptr[(b + 1) * a.G] - e0[k];
+      e0 = a.d_ptr[b * a.G];
+      len = a.d_ptr[(b + 1) * a.G] - e0;
     }
-    ce[k] = 0;
-    co[k] = 0;
+    stream_init(a, dmask, S[k], e0, len);
   }
-  const double4* mine = wsm + L.g * NearSmem::kSeg;
+  const double4* mine = wsm + L.g * NearSmem<CH>::kSeg;
   bool live = false;
 #pragma unroll
-  for (int k = 0; k < kGMax; ++k) live |= ce[k] < len[k];
+  for (int k = 0; k < kGMax; ++k) live |= S[k].e < S[k].len;
   if (live) {
     __syncwarp();
-    bool masked = near_stage(a, dmask, e0, len, ce, co, wsm, 0, lane);
+    bool masked = near_stage<CH>(a, dmask, S, wsm, 0, lane);
     for (int buf = 0;; buf ^= 1) {
       bool more = false;
 #pragma unroll
-      for (int k = 0; k < kGMax; ++k) more |= ce[k] < len[k];
+      for (int k = 0; k < kGMax; ++k) more |= S[k].e < S[k].len;
       bool masked_next = false;
       if (more) {
-        masked_next = near_stage(a, dmask, e0, len, ce, co, wsm, buf ^ 1, lane);
+        masked_next = near_stage<CH>(a, dmask, S, wsm, buf ^ 1, lane);
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
@@ -462,9 +547,9 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
       __syncwarp();
       double part[2] = {0.0, 0.0};
       if (masked)
-        near_chunk<KIND, true>(part, mine + buf * kNearCh, tx, ty, tz, a.kappa);
+        near_chunk<KIND, CH, true>(part, mine + buf * CH, tx, ty, tz, a.kappa);
       else
-        near_chunk<KIND, false>(part, mine + buf * kNearCh, tx, ty, tz, a.kappa);
+        near_chunk<KIND, CH, false>(part, mine + buf * CH, tx, ty, tz, a.kappa);
 #pragma unroll
       for (int t = 0; t < 2; ++t) neumaier(acc[t], comp[t], part[t]);
       __syncwarp();
@@ -486,19 +571,29 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
   }
 }
 
-template <int KIND, int MINB>
+template <int KIND, int CH, int MINB>
 __global__ void __launch_bounds__(kWarps * 32, MINB)
 k_near_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int32_t* poff,
               const uint8_t* dmask, int* counter) {
   extern __shared__ double4 nsmem[];
   double4* smem = nsmem;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double4* wsm = smem + warp * NearSmem::kWarp;
+  double4* wsm = smem + warp * NearSmem<CH>::kWarp;
   for (int item = next_item(counter); item < n_items; item = next_item(counter))
-    near_packed_item<KIND>(a, items[item], poff, dmask, wsm, lane);
+    near_packed_item<KIND, CH>(a, items[item], poff, dmask, wsm, lane);
 }
 
 // ---------------------------------------------------------------------------
+// Tuning switches for measurements (BLTC_FAR_UNROLL=1|3, BLTC_NEAR_CHUNK=32|64).
+int tune_far_unroll() {
+  const char* e = std::getenv("BLTC_FAR_UNROLL");
+  return e ? std::atoi(e) : 3;   // 3 rows per step: -2% far time at C4 (measured)
+}
+int tune_near_chunk() {
+  const char* e = std::getenv("BLTC_NEAR_CHUNK");
+  return e ? std::atoi(e) : kNearCh;
+}
+
 template <typename K>
 int persistent_grid(K kernel, int threads, size_t smem) {
   int dev = 0, sms = 0, per_sm = 0;
@@ -508,10 +603,10 @@ int persistent_grid(K kernel, int threads, size_t smem) {
   return sms * (per_sm > 0 ? per_sm : 1);
 }
 
-template <int KIND, int M>
+template <int KIND, int M, int KU = 1>
 void far_packed_launch(const EvalArgs& a, const PackedItems& it, int* counter, cudaStream_t st) {
   const size_t smem = sizeof(double) * kWarps * FarSmem<M>::kWarp;
-  auto kern = k_far_packed<KIND, M, 2>;
+  auto kern = k_far_packed<KIND, M, 2, KU>;
   BLTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = persistent_grid(kern, kWarps * 32, smem);
   kern<<<grid, kWarps * 32, smem, st>>>(a, it.items, it.n_items, it.poff, counter);
@@ -525,17 +620,20 @@ bool far_packed_dispatch(const EvalArgs& a, const PackedItems& it, int* counter,
     case 5: far_packed_launch<KIND, 5>(a, it, counter, st); return true;
     case 6: far_packed_launch<KIND, 6>(a, it, counter, st); return true;
     case 8: far_packed_launch<KIND, 8>(a, it, counter, st); return true;
-    case 9: far_packed_launch<KIND, 9>(a, it, counter, st); return true;
+    case 9:
+      if (KIND == 0 && tune_far_unroll() == 3) far_packed_launch<KIND, 9, 3>(a, it, counter, st);
+      else far_packed_launch<KIND, 9>(a, it, counter, st);
+      return true;
     case 11: far_packed_launch<KIND, 11>(a, it, counter, st); return true;
     default: return false;
   }
 }
 
-template <int KIND>
+template <int KIND, int CH = kNearCh>
 void near_packed_launch(const EvalArgs& a, const PackedItems& it, int* counter,
                         cudaStream_t st) {
-  const size_t smem = sizeof(double4) * kWarps * NearSmem::kWarp;
-  auto kern = k_near_packed<KIND, 2>;
+  const size_t smem = sizeof(double4) * kWarps * NearSmem<CH>::kWarp;
+  auto kern = k_near_packed<KIND, CH, 2>;
   BLTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = persistent_grid(kern, kWarps * 32, smem);
   kern<<<grid, kWarps * 32, smem, st>>>(a, it.items, it.n_items, it.poff, it.dmask, counter);
@@ -605,7 +703,8 @@ void launch_eval_packed(const EvalArgs& a, int kind, const PackedItems& it, int*
   if (kind == 0) far_packed_dispatch<0>(a, it, counters, st);
   else far_packed_dispatch<1>(a, it, counters, st);
   if (timing) BLTC_CUDA(cudaEventRecord(e1, st));
-  if (kind == 0) near_packed_launch<0>(a, it, counters + 1, st);
+  if (kind == 0 && tune_near_chunk() == 64) near_packed_launch<0, 64>(a, it, counters + 1, st);
+  else if (kind == 0) near_packed_launch<0>(a, it, counters + 1, st);
   else near_packed_launch<1>(a, it, counters + 1, st);
   if (timing) {
     BLTC_CUDA(cudaEventRecord(e2, st));
