@@ -49,19 +49,24 @@ __device__ __forceinline__ double rsqrt_fast(double x) {
 }
 
 // q / sqrt(d2) accumulated into acc (eval_fast.cu: one 3-register DFMA).
+// FORM 0: acc += (q y0) p.  FORM 2: acc += q (y0 p) -- the charge / moment
+// is the operand shared by a lane's two targets, so the second accumulating
+// DFMA can take it from the operand reuse cache (two register reads).
+template <int FORM>
 __device__ __forceinline__ double coulomb_acc(double acc, double q, double d2) {
   double y0;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(d2));
   const double e = fma(-__dmul_rn(d2, y0), y0, 1.0);
   const double c = fma(0.375, e, 0.5);
   const double p = fma(e, c, 1.0);
+  if (FORM == 2) return fma(q, __dmul_rn(y0, p), acc);
   const double qy = __dmul_rn(q, y0);
   return fma(qy, p, acc);
 }
 
-template <int KIND>
+template <int KIND, int FORM = 0>
 __device__ __forceinline__ double pair_acc(double acc, double q, double d2, double kappa) {
-  if (KIND == 0) return coulomb_acc(acc, q, d2);
+  if (KIND == 0) return coulomb_acc<FORM>(acc, q, d2);
   const double y = rsqrt_fast(d2);
   const double r = __dmul_rn(d2, y);
   return fma(__dmul_rn(q, exp(-kappa * r)), y, acc);
@@ -247,7 +252,7 @@ __device__ __forceinline__ void far_stage_slab(double* wsm, const FarHdr* H, int
   cp_async_commit();
 }
 
-template <int KIND, int M, int KU>
+template <int KIND, int M, int KU, int FORM>
 __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it,
                                                 const int32_t* poff, double* wsm, int lane) {
   using SM = FarSmem<M>;
@@ -345,7 +350,8 @@ __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it
           const double qv = qr[k3];
 #pragma unroll
           for (int t = 0; t < 2; ++t)
-            part[t] = pair_acc<KIND>(part[t], qv, __dadd_rn(dxy2[t], dz2[t][k3]), a.kappa);
+            part[t] = pair_acc<KIND, FORM>(part[t], qv, __dadd_rn(dxy2[t], dz2[t][k3]),
+                                           a.kappa);
         }
       }
       __syncwarp();
@@ -357,7 +363,7 @@ __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it
   if (L.v1) a.far_out[L.i1] = acc[1];
 }
 
-template <int KIND, int M, int MINB, int KU>
+template <int KIND, int M, int MINB, int KU, int FORM>
 __global__ void __launch_bounds__(kWarps * 32, MINB)
 k_far_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int32_t* poff,
              int* counter) {
@@ -365,7 +371,7 @@ k_far_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int3
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* wsm = smem + warp * FarSmem<M>::kWarp;
   for (int item = next_item(counter); item < n_items; item = next_item(counter))
-    far_packed_item<KIND, M, KU>(a, items[item], poff, wsm, lane);
+    far_packed_item<KIND, M, KU, FORM>(a, items[item], poff, wsm, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -377,7 +383,7 @@ struct NearSmem {
   static constexpr int kWarp = kGMax * kSeg;
 };
 
-template <int KIND, int CH, bool MASKED>
+template <int KIND, int CH, bool MASKED, int FORM>
 __device__ __forceinline__ void near_chunk(double (&part)[2], const double4* src,
                                            const double (&tx)[2], const double (&ty)[2],
                                            const double (&tz)[2], double kappa) {
@@ -393,9 +399,9 @@ __device__ __forceinline__ void near_chunk(double (&part)[2], const double4* src
       const double d2 = fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx)));
       if (MASKED) {
         const bool ok = __double_as_longlong(d2) >= tb;
-        part[t] = pair_acc<KIND>(part[t], ok ? s.w : 0.0, ok ? d2 : 1.0, kappa);
+        part[t] = pair_acc<KIND, FORM>(part[t], ok ? s.w : 0.0, ok ? d2 : 1.0, kappa);
       } else {
-        part[t] = pair_acc<KIND>(part[t], s.w, d2, kappa);
+        part[t] = pair_acc<KIND, FORM>(part[t], s.w, d2, kappa);
       }
     }
   }
@@ -505,7 +511,7 @@ __device__ __forceinline__ bool near_stage(const EvalArgs& a, const uint8_t* dma
   return __any_sync(0xffffffffu, need_mask);
 }
 
-template <int KIND, int CH>
+template <int KIND, int CH, int FORM>
 __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 it,
                                                  const int32_t* poff, const uint8_t* dmask,
                                                  double4* wsm, int lane) {
@@ -547,9 +553,9 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
       __syncwarp();
       double part[2] = {0.0, 0.0};
       if (masked)
-        near_chunk<KIND, CH, true>(part, mine + buf * CH, tx, ty, tz, a.kappa);
+        near_chunk<KIND, CH, true, FORM>(part, mine + buf * CH, tx, ty, tz, a.kappa);
       else
-        near_chunk<KIND, CH, false>(part, mine + buf * CH, tx, ty, tz, a.kappa);
+        near_chunk<KIND, CH, false, FORM>(part, mine + buf * CH, tx, ty, tz, a.kappa);
 #pragma unroll
       for (int t = 0; t < 2; ++t) neumaier(acc[t], comp[t], part[t]);
       __syncwarp();
@@ -571,7 +577,7 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
   }
 }
 
-template <int KIND, int CH, int MINB>
+template <int KIND, int CH, int MINB, int FORM>
 __global__ void __launch_bounds__(kWarps * 32, MINB)
 k_near_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int32_t* poff,
               const uint8_t* dmask, int* counter) {
@@ -580,18 +586,22 @@ k_near_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double4* wsm = smem + warp * NearSmem<CH>::kWarp;
   for (int item = next_item(counter); item < n_items; item = next_item(counter))
-    near_packed_item<KIND, CH>(a, items[item], poff, dmask, wsm, lane);
+    near_packed_item<KIND, CH, FORM>(a, items[item], poff, dmask, wsm, lane);
 }
 
 // ---------------------------------------------------------------------------
-// Tuning switches for measurements (BLTC_FAR_UNROLL=1|3, BLTC_NEAR_CHUNK=32|64).
+// Tuning switches for measurements (BLTC_FAR_UNROLL=1|3, BLTC_PFORM=0|2).
 int tune_far_unroll() {
   const char* e = std::getenv("BLTC_FAR_UNROLL");
   return e ? std::atoi(e) : 3;   // 3 rows per step: -2% far time at C4 (measured)
 }
-int tune_near_chunk() {
-  const char* e = std::getenv("BLTC_NEAR_CHUNK");
-  return e ? std::atoi(e) : kNearCh;
+int tune_form() {
+  const char* e = std::getenv("BLTC_PFORM");
+  return e ? std::atoi(e) : 2;   // FORM 2: -0.9% far, -1.5% near at C4 (measured)
+}
+int tune_far_minb() {
+  const char* e = std::getenv("BLTC_FAR_MINB");
+  return e ? std::atoi(e) : 2;
 }
 
 template <typename K>
@@ -603,10 +613,10 @@ int persistent_grid(K kernel, int threads, size_t smem) {
   return sms * (per_sm > 0 ? per_sm : 1);
 }
 
-template <int KIND, int M, int KU = 1>
+template <int KIND, int M, int KU = 1, int FORM = 0, int MINB = 2>
 void far_packed_launch(const EvalArgs& a, const PackedItems& it, int* counter, cudaStream_t st) {
   const size_t smem = sizeof(double) * kWarps * FarSmem<M>::kWarp;
-  auto kern = k_far_packed<KIND, M, 2, KU>;
+  auto kern = k_far_packed<KIND, M, MINB, KU, FORM>;
   BLTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = persistent_grid(kern, kWarps * 32, smem);
   kern<<<grid, kWarps * 32, smem, st>>>(a, it.items, it.n_items, it.poff, counter);
@@ -621,7 +631,10 @@ bool far_packed_dispatch(const EvalArgs& a, const PackedItems& it, int* counter,
     case 6: far_packed_launch<KIND, 6>(a, it, counter, st); return true;
     case 8: far_packed_launch<KIND, 8>(a, it, counter, st); return true;
     case 9:
-      if (KIND == 0 && tune_far_unroll() == 3) far_packed_launch<KIND, 9, 3>(a, it, counter, st);
+      if (KIND == 0 && tune_form() == 2 && tune_far_minb() == 1)
+        far_packed_launch<KIND, 9, 3, 2, 1>(a, it, counter, st);
+      else if (KIND == 0 && tune_form() == 2) far_packed_launch<KIND, 9, 3, 2>(a, it, counter, st);
+      else if (KIND == 0 && tune_far_unroll() == 3) far_packed_launch<KIND, 9, 3>(a, it, counter, st);
       else far_packed_launch<KIND, 9>(a, it, counter, st);
       return true;
     case 11: far_packed_launch<KIND, 11>(a, it, counter, st); return true;
@@ -629,11 +642,11 @@ bool far_packed_dispatch(const EvalArgs& a, const PackedItems& it, int* counter,
   }
 }
 
-template <int KIND, int CH = kNearCh>
+template <int KIND, int CH = kNearCh, int FORM = 0>
 void near_packed_launch(const EvalArgs& a, const PackedItems& it, int* counter,
                         cudaStream_t st) {
   const size_t smem = sizeof(double4) * kWarps * NearSmem<CH>::kWarp;
-  auto kern = k_near_packed<KIND, CH, 2>;
+  auto kern = k_near_packed<KIND, CH, 2, FORM>;
   BLTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = persistent_grid(kern, kWarps * 32, smem);
   kern<<<grid, kWarps * 32, smem, st>>>(a, it.items, it.n_items, it.poff, it.dmask, counter);
@@ -703,7 +716,7 @@ void launch_eval_packed(const EvalArgs& a, int kind, const PackedItems& it, int*
   if (kind == 0) far_packed_dispatch<0>(a, it, counters, st);
   else far_packed_dispatch<1>(a, it, counters, st);
   if (timing) BLTC_CUDA(cudaEventRecord(e1, st));
-  if (kind == 0 && tune_near_chunk() == 64) near_packed_launch<0, 64>(a, it, counters + 1, st);
+  if (kind == 0 && tune_form() == 2) near_packed_launch<0, kNearCh, 2>(a, it, counters + 1, st);
   else if (kind == 0) near_packed_launch<0>(a, it, counters + 1, st);
   else near_packed_launch<1>(a, it, counters + 1, st);
   if (timing) {
