@@ -56,54 +56,91 @@ __global__ void k_init_boxes(unsigned long long* box_u, int64_t begin, int64_t e
 }
 
 // Minimal bounding boxes (tree.py:138-141): exact min/max via order-preserving
-// integer atomics; warp-aggregated when all 32 lanes share a node.
+// integer atomics.  After the level's scatter the particles of every node are
+// contiguous, so each warp walks a contiguous chunk of kBoxChunk particles
+// keeping per-lane running min/max for the node it is in, and reduces and
+// flushes them (6 atomics) only when the node changes: one flush per node
+// boundary instead of one per 32 particles, which removes the same-address
+// atomic contention on large nodes.  Particles in finished leaves carry
+// node -1 and are skipped.
+constexpr int kBoxChunk = 32 * 16;
+
+__device__ __forceinline__ void box_flush(int nd, unsigned long long (&mn)[3],
+                                          unsigned long long (&mx)[3],
+                                          unsigned long long* box_u, int lane) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const unsigned long long a = __shfl_xor_sync(0xffffffffu, mn[d], o);
+      const unsigned long long b = __shfl_xor_sync(0xffffffffu, mx[d], o);
+      mn[d] = a < mn[d] ? a : mn[d];
+      mx[d] = b > mx[d] ? b : mx[d];
+    }
+  }
+  if (lane == 0 && nd >= 0 && mx[0] != 0ull) {
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      atomicMin(&box_u[(int64_t)nd * 6 + d], mn[d]);
+      atomicMax(&box_u[(int64_t)nd * 6 + 3 + d], mx[d]);
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    mn[d] = ~0ull;
+    mx[d] = 0ull;
+  }
+}
+
 __global__ void k_box(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
                       const double* __restrict__ z, const int32_t* __restrict__ node_of,
                       unsigned long long* box_u) {
   const int lane = threadIdx.x & 31;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n;
-       base += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = base + threadIdx.x;
-    bool valid = i < n;
-    int nd = valid ? node_of[i] : -1;
-    unsigned long long v[3];
-    if (valid) {
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t c0 = warp * kBoxChunk;
+  if (c0 >= n) return;
+  const int64_t c1 = min(c0 + kBoxChunk, n);
+  unsigned long long mn[3] = {~0ull, ~0ull, ~0ull}, mx[3] = {0ull, 0ull, 0ull};
+  int cur = node_of[c0];   // warp-uniform: node being accumulated
+  for (int64_t base = c0; base < c1; base += 32) {
+    const int64_t i = base + lane;
+    const bool valid = i < c1;
+    const int nd = valid ? node_of[i] : cur;
+    unsigned long long v[3] = {0ull, 0ull, 0ull};
+    if (valid && nd >= 0) {
       v[0] = d2ord(x[i]);
       v[1] = d2ord(y[i]);
       v[2] = d2ord(z[i]);
     }
-    int nd0 = __shfl_sync(0xffffffffu, nd, 0);
-    bool uniform = __all_sync(0xffffffffu, valid && nd == nd0);
-    if (uniform) {
-      if (nd0 < 0) continue;
-      unsigned long long mn[3], mx[3];
+    const bool mine = valid && nd == cur;
+    if (mine) {
 #pragma unroll
-      for (int d = 0; d < 3; ++d) { mn[d] = v[d]; mx[d] = v[d]; }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          unsigned long long a = __shfl_xor_sync(0xffffffffu, mn[d], o);
-          unsigned long long b = __shfl_xor_sync(0xffffffffu, mx[d], o);
-          mn[d] = a < mn[d] ? a : mn[d];
-          mx[d] = b > mx[d] ? b : mx[d];
-        }
+      for (int d = 0; d < 3; ++d) {
+        mn[d] = v[d] < mn[d] ? v[d] : mn[d];
+        mx[d] = v[d] > mx[d] ? v[d] : mx[d];
       }
-      if (lane == 0) {
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          atomicMin(&box_u[(int64_t)nd0 * 6 + d], mn[d]);
-          atomicMax(&box_u[(int64_t)nd0 * 6 + 3 + d], mx[d]);
-        }
-      }
-    } else if (valid && nd >= 0) {
+    }
+    if (__all_sync(0xffffffffu, !valid || nd == cur)) continue;
+    // node boundary inside these 32 particles
+    box_flush(cur, mn, mx, box_u, lane);
+    const int last = __shfl_sync(0xffffffffu, nd, 31);   // invalid lanes hold cur
+    if (valid && nd >= 0 && nd != cur && nd != last) {   // nodes wholly inside: rare
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
         atomicMin(&box_u[(int64_t)nd * 6 + d], v[d]);
         atomicMax(&box_u[(int64_t)nd * 6 + 3 + d], v[d]);
       }
     }
+    if (valid && nd == last && last != cur) {
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        mn[d] = v[d];
+        mx[d] = v[d];
+      }
+    }
+    cur = last;
   }
+  box_flush(cur, mn, mx, box_u, lane);
 }
 
 __global__ void k_finalize_boxes(const unsigned long long* box_u, double* lo, double* hi,
@@ -459,7 +496,8 @@ void build_partition(Partition& P, BuildScratch& S, int64_t n, const double* dx,
   BLTC_LAUNCH_CHECK();
   k_init_boxes<<<1, 32, 0, st>>>(S.box_u.p, 0, 1);
   BLTC_LAUNCH_CHECK();
-  k_box<<<std::min(grid_for(n, 256), 148 * 8), 256, 0, st>>>(n, cx, cy, cz, cn, S.box_u.p);
+  k_box<<<grid_for((n + kBoxChunk - 1) / kBoxChunk * 32, 256), 256, 0, st>>>(n, cx, cy, cz, cn,
+                                                                          S.box_u.p);
   BLTC_LAUNCH_CHECK();
   k_finalize_boxes<<<1, 32, 0, st>>>(S.box_u.p, P.lo.p, P.hi.p, 0, 1);
   BLTC_LAUNCH_CHECK();
@@ -507,7 +545,8 @@ void build_partition(Partition& P, BuildScratch& S, int64_t n, const double* dx,
     const int64_t nb = end, ne = end + total_children;
     k_init_boxes<<<grid_for(ne - nb, 128), 128, 0, st>>>(S.box_u.p, nb, ne);
     BLTC_LAUNCH_CHECK();
-    k_box<<<std::min(grid_for(n, 256), 148 * 8), 256, 0, st>>>(n, cx, cy, cz, cn, S.box_u.p);
+    k_box<<<grid_for((n + kBoxChunk - 1) / kBoxChunk * 32, 256), 256, 0, st>>>(n, cx, cy, cz, cn,
+                                                                          S.box_u.p);
     BLTC_LAUNCH_CHECK();
     k_finalize_boxes<<<grid_for(ne - nb, 128), 128, 0, st>>>(S.box_u.p, P.lo.p, P.hi.p, nb, ne);
     BLTC_LAUNCH_CHECK();
