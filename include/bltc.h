@@ -171,6 +171,20 @@ BLTC_API int bltc_rank_evaluate(bltc_ctx* ctx, const bltc_params* p, int32_t ran
                        const double* const* particles, const double* const* moments,
                        double* phi_out, int32_t device_ptrs, bltc_stats* stats);
 
+/* LET step one (decomp.py:354-379, build_let): the interaction lists of this
+ * rank's batches against every owner's published tree records (device
+ * pointers, owner order 0..R-1; only the geometry / count / child fields are
+ * read).  flags_out (device, int32, sum of n_clusters, owner order 0..R-1,
+ * zeroed here): bit 0 = some batch approximates the cluster (its moment row
+ * is needed), bit 1 = some batch sums it directly (its particles are
+ * needed).  Step two (fetching exactly those rows and slices) is the
+ * caller's exchange; the fetched data, with the records' particle ranges and
+ * moment rows remapped into the fetched buffers, then go to
+ * bltc_rank_evaluate unchanged. */
+BLTC_API int bltc_rank_needs(bltc_ctx* ctx, const bltc_params* p, int32_t ranks, int32_t my_rank,
+                             const int64_t* n_clusters, const double* const* records,
+                             int32_t* flags_out);
+
 /* ---- Verification oracle on the device (cli.py:73-149) --
  * Brute-force Neumaier direct sums at the targets idx[0..n_idx) (indices into
  * tx/ty/tz; NULL idx = all n_t targets) over all sources, singular pairs

@@ -168,6 +168,12 @@ __global__ void k_pack_records(int64_t nn, const double* lo, const double* hi,
   r[17] = 0.0;
 }
 
+// LET step one: flag every forest cluster some list entry references.
+__global__ void k_mark_needs(int64_t n, const int32_t* __restrict__ idx, int bit, int32_t* flags) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) atomicOr(&flags[idx[i]], bit);
+}
+
 // One owner's records -> the forest's MacNode / EvalCluster arrays, shifting
 // particle ranges and moment rows by the owner's offsets in the forest.
 __global__ void k_unpack_records(int64_t nn, const double* rec, int32_t p_off, int32_t row_off,
@@ -234,6 +240,7 @@ struct bltc_ctx {
   DBuf<int2> items, items2;
   DBuf<int32_t> pk_pc, pk_poff, pk_wcnt, pk_woff;   // packed FAST items
   DBuf<int4> pk_items;
+  DBuf<int32_t> need;   // LET step one flags (bltc_rank_needs)
   DBuf<uint8_t> pk_dmask;
   DBuf<double> partial;
   DBuf<double2> dpartial;
@@ -733,7 +740,7 @@ int bltc_destroy(bltc_ctx* c) {
     c->widen.release(); c->item_cnt.release(); c->item_off.release(); c->counters.release();
     c->items.release(); c->items2.release();
     c->pk_pc.release(); c->pk_poff.release(); c->pk_wcnt.release(); c->pk_woff.release();
-    c->pk_items.release(); c->pk_dmask.release(); c->partial.release(); c->dpartial.release();
+    c->pk_items.release(); c->pk_dmask.release(); c->need.release(); c->partial.release(); c->dpartial.release();
     c->didx.release(); c->dout.release(); c->f_ecl.release(); c->f_mac.release(); c->f_x.release();
     c->f_y.release(); c->f_z.release(); c->f_q.release(); c->f_rows.release();
     c->f_src4.release();
@@ -1034,6 +1041,77 @@ int bltc_rank_publish(bltc_ctx* c, double* records, double* particles, double* m
     if (c->n_moments > 0)
       BLTC_CUDA(cudaMemcpyAsync(moments, c->rows.p, c->n_moments * mstride * sizeof(double),
                                 cudaMemcpyDeviceToDevice, st));
+    BLTC_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int bltc_rank_needs(bltc_ctx* c, const bltc_params* p, int32_t ranks, int32_t my_rank,
+                    const int64_t* n_clusters, const double* const* records, int32_t* flags_out) {
+  return guarded([&] {
+    if (!c || !c->rank_built) {
+      set_error("bltc_rank_build has not run on this context");
+      throw UserError{BLTC_ERR_STATE};
+    }
+    BLTC_CUDA(cudaSetDevice(c->device));
+    check_params(p);
+    if (ranks < 1 || my_rank < 0 || my_rank >= ranks) {
+      set_error("invalid ranks / my_rank");
+      throw UserError{BLTC_ERR_VALUE};
+    }
+    if (p->degree != c->params.degree || p->leaf_size != c->params.leaf_size ||
+        p->batch_size != c->params.batch_size) {
+      set_error("list parameters differ from those of bltc_rank_build");
+      throw UserError{BLTC_ERR_VALUE};
+    }
+    cudaStream_t st = c->st;
+    std::vector<int> owners;
+    owners.push_back(my_rank);
+    for (int o = 0; o < ranks; ++o)
+      if (o != my_rank) owners.push_back(o);
+    const int G = ranks;
+    std::vector<int32_t> cl_off(G), rank_off(ranks);
+    int64_t C = 0;
+    for (int g = 0; g < G; ++g) {
+      cl_off[g] = (int32_t)C;
+      C += n_clusters[owners[g]];
+    }
+    int64_t R0 = 0;
+    for (int o = 0; o < ranks; ++o) {
+      rank_off[o] = (int32_t)R0;
+      R0 += n_clusters[o];
+    }
+    c->f_mac.resize(C);
+    c->f_ecl.resize(C);
+    std::vector<const MacNode*> trees(G);
+    for (int g = 0; g < G; ++g) {
+      const int64_t nc = n_clusters[owners[g]];
+      k_unpack_records<<<grid_for(nc, 128), 128, 0, st>>>(nc, records[owners[g]], 0, 0,
+                                                          c->f_mac.p + cl_off[g],
+                                                          c->f_ecl.p + cl_off[g]);
+      BLTC_LAUNCH_CHECK();
+      trees[g] = c->f_mac.p + cl_off[g];
+    }
+    build_lists(c, p, G, trees.data(), cl_off.data());
+    c->need.resize(C + 1);
+    BLTC_CUDA(cudaMemsetAsync(c->need.p, 0, (C + 1) * sizeof(int32_t), st));
+    const Lists& L = c->lists;
+    if (L.n_approx > 0) {
+      k_mark_needs<<<grid_for(L.n_approx, 256), 256, 0, st>>>(L.n_approx, L.a_idx.p, 1,
+                                                               c->need.p);
+      BLTC_LAUNCH_CHECK();
+    }
+    if (L.n_direct > 0) {
+      k_mark_needs<<<grid_for(L.n_direct, 256), 256, 0, st>>>(L.n_direct, L.d_idx.p, 2,
+                                                               c->need.p);
+      BLTC_LAUNCH_CHECK();
+    }
+    for (int g = 0; g < G; ++g) {
+      const int o = owners[g];
+      if (n_clusters[o] > 0)
+        BLTC_CUDA(cudaMemcpyAsync(flags_out + rank_off[o], c->need.p + cl_off[g],
+                                  n_clusters[o] * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                                  st));
+    }
     BLTC_CUDA(cudaStreamSynchronize(st));
   });
 }

@@ -11,10 +11,18 @@ replicated by ONE all-gather of the published records (NCCL over NVLink when
 its batches against the local tree first and the remote trees in ascending
 owner order (decomp.py:437-454), exactly the reference's accumulation order.
 
-Replicating the whole forest replaces the reference's two-step one-sided LET
-fetch (decomp.py:354-399): every rank holds a superset of its locally
-essential tree, so the reference's sufficiency property holds trivially and
-the evaluation is unchanged.  A LET-minimal exchange is SURVEY.md 8(f) #2.
+Exchange (``exchange=``):
+* ``"let"`` (default) -- the reference's two-step locally essential tree
+  (decomp.py:354-399, build_let) as collectives: (1) all-gather of every
+  rank's tree records; each rank builds its batches' interaction lists
+  against every remote tree on its GPU (``bltc_rank_needs``) and marks the
+  clusters it approximates (moment rows needed) or sums directly (particle
+  slices needed); (2) one all-to-all of the requested cluster ids and one
+  all-to-all of exactly those moment rows and particle slices.  Nothing else
+  moves, so the fetch statistics are the reference's (``let_violations``
+  counts stay zero) and the evaluation sees the same data as the reference.
+* ``"replicate"`` -- one all-gather of the whole forest (every rank holds a
+  superset of its LET; cheaper to orchestrate on one NVSwitch box).
 
 Execution models:
 * ``torch.distributed`` initialised with world_size == ranks: this process is
@@ -178,6 +186,193 @@ def all_gather_published(pub: Published, ranks: int, group=None) -> list[Publish
     return out
 
 
+def all_gather_records(pub: Published, ranks: int, group=None) -> list:
+    """LET step one's collective: every rank's tree records on every rank
+    (one size all-gather, one padded all-gather)."""
+    import torch
+    import torch.distributed as dist
+
+    dev = pub.records.device
+    n = torch.tensor([pub.records.shape[0]], dtype=torch.int64, device=dev)
+    sizes = [torch.empty_like(n) for _ in range(ranks)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(v.item()) for v in sizes]
+    cap = max(1, max(sizes)) * RECORD_DOUBLES
+    buf = torch.zeros(cap, dtype=torch.float64, device=dev)
+    buf[:pub.records.numel()] = pub.records.reshape(-1)
+    gathered = [torch.empty_like(buf) for _ in range(ranks)]
+    dist.all_gather(gathered, buf, group=group)
+    return [gathered[r][:sizes[r] * RECORD_DOUBLES].view(sizes[r], RECORD_DOUBLES)
+            for r in range(ranks)]
+
+
+def let_request(flags) -> tuple:
+    """Cluster ids one origin needs from one owner, each sorted ascending as
+    in build_let (decomp.py:372-373): (moment-row ids, particle-slice ids)."""
+    import torch
+    f = flags.to(torch.int64)
+    a = torch.nonzero(f & 1).reshape(-1)
+    d = torch.nonzero(f & 2).reshape(-1)
+    return a, d
+
+
+def _slice_index(records, d_ids):
+    """Concatenated particle indices of the clusters d_ids (list order)."""
+    import torch
+    dev = records.device
+    if d_ids.numel() == 0:
+        return torch.zeros(0, dtype=torch.int64, device=dev), torch.zeros(0, dtype=torch.int64,
+                                                                          device=dev)
+    st = records[d_ids, 14].to(torch.int64)
+    sz = records[d_ids, 15].to(torch.int64) - st
+    off = torch.cumsum(sz, 0) - sz
+    total = int(sz.sum().item())
+    seg = torch.repeat_interleave(torch.arange(d_ids.numel(), device=dev), sz)
+    idx = st[seg] + (torch.arange(total, device=dev) - off[seg])
+    return idx, sz
+
+
+def let_serve(pub: Published, a_ids, d_ids):
+    """Owner side of step two: the requested moment rows and particle slices,
+    flattened into one float64 buffer (rows first)."""
+    import torch
+    mrow = pub.records[a_ids, 16].to(torch.int64)
+    rows = pub.moments[mrow] if a_ids.numel() else pub.moments[:0]
+    idx, _ = _slice_index(pub.records, d_ids)
+    par = pub.particles[:, idx]
+    return torch.cat([rows.reshape(-1), par.reshape(-1)])
+
+
+def let_payload_size(records, a_ids, d_ids, ncols: int) -> int:
+    import torch
+    p = 0
+    if d_ids.numel():
+        p = int((records[d_ids, 15] - records[d_ids, 14]).to(torch.int64).sum().item())
+    return int(a_ids.numel()) * ncols + 4 * p
+
+
+def let_assemble(records, a_ids, d_ids, payload, ncols: int):
+    """Origin side of step two: the owner's fetched data as a Published whose
+    records point into the fetched buffers (moment row -> index among the
+    fetched rows, particle range -> offset in the fetched slices; records of
+    clusters not fetched keep no data).  Returns (Published, FetchStats)."""
+    import torch
+    na = int(a_ids.numel())
+    rows = payload[:na * ncols].view(na, ncols)
+    _, sz = _slice_index(records, d_ids)
+    P = int(sz.sum().item()) if sz.numel() else 0
+    par = payload[na * ncols:na * ncols + 4 * P].view(4, P)
+    rec = records.clone()
+    rec[:, 14] = 0.0
+    rec[:, 15] = 0.0
+    rec[:, 16] = -1.0
+    if na:
+        rec[a_ids, 16] = torch.arange(na, dtype=rec.dtype, device=rec.device)
+    if d_ids.numel():
+        off = torch.cumsum(sz, 0) - sz
+        rec[d_ids, 14] = off.to(rec.dtype)
+        rec[d_ids, 15] = (off + sz).to(rec.dtype)
+    both = torch.unique(torch.cat([a_ids, d_ids]))
+    fs = FetchStats(tree_records=int(records.shape[0]), clusters=int(both.numel()),
+                    moments=na, particles=P)
+    return Published(rec, par, rows), fs
+
+
+def let_exchange(pub: Published, needs_fn, ranks: int, me: int, group=None):
+    """Both LET steps over a process group (NCCL for CUDA tensors): returns
+    (forest in owner order -- own data for ``me``, fetched data otherwise --
+    and {(me, owner): FetchStats})."""
+    import torch
+    import torch.distributed as dist
+
+    dev = pub.records.device
+    ncols = int(pub.moments.shape[1])
+    records = all_gather_records(pub, ranks, group)
+    flags = needs_fn(records)
+    req = {o: let_request(flags[o]) for o in range(ranks) if o != me}
+    # requests: counts, then ids
+    cnt = torch.zeros((ranks, 2), dtype=torch.int64, device=dev)
+    for o, (a, d) in req.items():
+        cnt[o, 0], cnt[o, 1] = a.numel(), d.numel()
+    rcnt = torch.empty_like(cnt)
+    dist.all_to_all_single(rcnt, cnt, group=group)
+    send_ids = torch.cat([torch.cat(req[o]) if o in req else
+                          torch.zeros(0, dtype=torch.int64, device=dev) for o in range(ranks)])
+    in_split = [int(cnt[o].sum().item()) for o in range(ranks)]
+    out_split = [int(rcnt[o].sum().item()) for o in range(ranks)]
+    recv_ids = torch.empty(sum(out_split), dtype=torch.int64, device=dev)
+    dist.all_to_all_single(recv_ids, send_ids, out_split, in_split, group=group)
+    # serve every requester
+    parts, serve_split, pos = [], [], 0
+    for r in range(ranks):
+        na, nd = int(rcnt[r, 0].item()), int(rcnt[r, 1].item())
+        ids = recv_ids[pos:pos + na + nd]
+        pos += na + nd
+        if r == me or na + nd == 0:
+            serve_split.append(0)
+            continue
+        buf = let_serve(pub, ids[:na], ids[na:])
+        parts.append(buf)
+        serve_split.append(int(buf.numel()))
+    send = torch.cat(parts) if parts else torch.zeros(0, dtype=torch.float64, device=dev)
+    fetch_split = [let_payload_size(records[o], *req[o], ncols) if o in req else 0
+                   for o in range(ranks)]
+    recv = torch.empty(sum(fetch_split), dtype=torch.float64, device=dev)
+    dist.all_to_all_single(recv, send, fetch_split, serve_split, group=group)
+    forest, fetch, pos = [], {}, 0
+    for o in range(ranks):
+        if o == me:
+            forest.append(pub)
+            continue
+        payload = recv[pos:pos + fetch_split[o]]
+        pos += fetch_split[o]
+        p_o, fs = let_assemble(records[o], *req[o], payload, ncols)
+        forest.append(p_o)
+        fetch[(me, o)] = fs
+    return forest, fetch
+
+
+def let_local(pubs: dict, needs_fns: dict, ranks: int):
+    """Both LET steps for ranks simulated in one process (no process group):
+    the same request / serve / assemble path, handed over in place."""
+    ncols = int(pubs[0].moments.shape[1])
+    records = [pubs[r].records for r in range(ranks)]
+    forests, fetch = {}, {}
+    for me in range(ranks):
+        flags = needs_fns[me](records)
+        forest = []
+        for o in range(ranks):
+            if o == me:
+                forest.append(pubs[me])
+                continue
+            a, d = let_request(flags[o])
+            payload = let_serve(pubs[o], a, d)
+            p_o, fs = let_assemble(records[o], a, d, payload, ncols)
+            forest.append(p_o)
+            fetch[(me, o)] = fs
+        forests[me] = forest
+    return forests, fetch
+
+
+def let_violations(forest: list, flags: list, me: int) -> dict:
+    """decomp.py:402-418: sufficiency (a referenced cluster without its data)
+    and minimality (data fetched that no batch references), from one origin's
+    fetched forest and its need flags."""
+    import torch
+    suff = mini = 0
+    for o, p in enumerate(forest):
+        if o == me:
+            continue
+        f = flags[o].to(torch.int64)
+        has_row = p.records[:, 16] >= 0
+        has_par = p.records[:, 15] > p.records[:, 14]
+        need_a = (f & 1) != 0
+        need_d = ((f & 2) != 0) & (p.records[:, 10] > 0)
+        suff += int((need_a & ~has_row).sum().item()) + int((need_d & ~has_par).sum().item())
+        mini += int((has_row & ~need_a).sum().item()) + int((has_par & ~need_d).sum().item())
+    return {"sufficiency": suff, "minimality": mini}
+
+
 # ---------------------------------------------------------------------------
 # The product rank engine: libbltc on one CUDA device
 
@@ -219,6 +414,21 @@ class DeviceRankEngine:
         torch.cuda.synchronize(dev)
         return Published(rec, par, mom[:sz["n_moment_rows"]])
 
+    def needs(self, ranks: int, my_rank: int, records: list) -> list:
+        """LET step one on the device: per owner, int32 need flags per cluster."""
+        torch = self.torch
+        dev = torch.device("cuda", self.device)
+        sizes = [int(r.shape[0]) for r in records]
+        recs = [r.to(dev).contiguous() for r in records]
+        flags = torch.empty(max(1, sum(sizes)), dtype=torch.int32, device=dev)
+        self.ctx.rank_needs(self.params, ranks, my_rank, sizes, [r.data_ptr() for r in recs],
+                            flags.data_ptr())
+        out, pos = [], 0
+        for n in sizes:
+            out.append(flags[pos:pos + n])
+            pos += n
+        return out
+
     def evaluate(self, ranks: int, my_rank: int, forest: list[Published]):
         torch = self.torch
         dev = torch.device("cuda", self.device)
@@ -241,8 +451,9 @@ class DeviceRankEngine:
 
 @dataclass(eq=False)
 class FetchStats:
-    """Per (origin, owner) exchange volume (decomp.py:324-331).  With the
-    replicated forest every origin receives the owner's whole tree."""
+    """Per (origin, owner) exchange volume (decomp.py:324-331): the reference's
+    LET counts with exchange="let"; with "replicate" every origin receives
+    the owner's whole tree."""
 
     tree_records: int = 0
     clusters: int = 0
@@ -286,14 +497,17 @@ def _process_group_world(group):
 
 
 def run_distributed(system, config, ranks: int, threads: int = 1, mode: str | None = None,
-                    group=None, engine_factory=None):
+                    group=None, engine_factory=None, exchange: str = "let"):
     """decomp.py:483-593 on GPUs.  Returns (phi in original order, stats) on
-    every participating process.  ``threads`` is accepted and ignored."""
+    every participating process.  ``threads`` is accepted and ignored;
+    ``exchange`` is "let" (the reference's minimal fetch) or "replicate"."""
     import time
 
     import torch
 
     del threads
+    if exchange not in ("let", "replicate"):
+        raise ValueError(f"exchange must be 'let' or 'replicate', got {exchange!r}")
     if not system.coincident:
         raise ValueError("distributed runs require targets and sources "
                          "to be the same particle set")
@@ -318,10 +532,18 @@ def run_distributed(system, config, ranks: int, threads: int = 1, mode: str | No
     t_build = time.perf_counter() - t0
     t0 = time.perf_counter()
     pubs = {r: engines[r].publish() for r in mine}
-    if world > 1:
-        forest = all_gather_published(pubs[me], ranks, group)
+    fetch = {}
+    if exchange == "let" and world > 1:
+        f, fetch = let_exchange(pubs[me], lambda recs: engines[me].needs(ranks, me, recs),
+                                ranks, me, group)
+        forests = {me: f}
+    elif exchange == "let":
+        needs = {r: (lambda recs, r=r: engines[r].needs(ranks, r, recs)) for r in mine}
+        forests, fetch = let_local(pubs, needs, ranks)
+    elif world > 1:
+        forests = {me: all_gather_published(pubs[me], ranks, group)}
     else:
-        forest = [pubs[r] for r in range(ranks)]
+        forests = {r: [pubs[o] for o in range(ranks)] for r in mine}
     t_exchange = time.perf_counter() - t0
     for r in mine:
         timings[r][2] = t_exchange
@@ -329,7 +551,7 @@ def run_distributed(system, config, ranks: int, threads: int = 1, mode: str | No
     rank_phi = {}
     for r in mine:
         tr = time.perf_counter()
-        rank_phi[r] = engines[r].evaluate(ranks, r, forest)
+        rank_phi[r] = engines[r].evaluate(ranks, r, forests[r])
         timings[r][3] = time.perf_counter() - tr
     t_eval = time.perf_counter() - t0
 
@@ -355,13 +577,13 @@ def run_distributed(system, config, ranks: int, threads: int = 1, mode: str | No
     else:
         for o in range(ranks):
             phi[part.rank_indices(o)] = rank_phi[o].detach().cpu().numpy()
-    fetch = {}
-    for r in mine:
-        for o in range(ranks):
-            if o != r:
-                nc, n, nrow = forest[o].sizes
-                fetch[(r, o)] = FetchStats(tree_records=nc, clusters=nc, moments=nrow,
-                                           particles=n)
+    if exchange == "replicate":
+        for r in mine:
+            for o in range(ranks):
+                if o != r:
+                    nc, n, nrow = forests[r][o].sizes
+                    fetch[(r, o)] = FetchStats(tree_records=nc, clusters=nc, moments=nrow,
+                                               particles=n)
     total = time.perf_counter() - t_start
     stats = DistributedStats(
         n_ranks=ranks, rank_counts=part.counts, n_clusters=int(local[2]),
@@ -379,7 +601,8 @@ class DeviceRankRunner:
     evaluation -- local tree / batches / moments, the forest all-gather over
     NCCL, evaluation of the local batches -- and returns the rank's stats."""
 
-    def __init__(self, ctx, system, config, mode: str | None = None, group=None):
+    def __init__(self, ctx, system, config, mode: str | None = None, group=None,
+                 exchange: str = "let"):
         import torch
         import torch.distributed as dist
         self.dist, self.group = dist, group
@@ -393,11 +616,18 @@ class DeviceRankRunner:
                        for a in (src.x, src.y, src.z, system.charges)]
         self.engine = DeviceRankEngine(config, mode, context=ctx)
         self.n_local = int(idx.shape[0])
+        self.exchange = exchange
         self.phi = None
+        self.fetch = {}
 
     def step(self):
         self.engine.build(*self.inputs)
         pub = self.engine.publish()
-        forest = all_gather_published(pub, self.ranks, self.group)
+        if self.exchange == "let":
+            forest, self.fetch = let_exchange(
+                pub, lambda recs: self.engine.needs(self.ranks, self.me, recs), self.ranks,
+                self.me, self.group)
+        else:
+            forest = all_gather_published(pub, self.ranks, self.group)
         self.phi = self.engine.evaluate(self.ranks, self.me, forest)
         return self.engine.stats

@@ -233,6 +233,17 @@ class Context:
             _lib.i64p(nrow), rec, par, mom, out, 1 if device_ptrs else 0, ctypes.byref(st)))
         return RunStats.from_c(st)
 
+    def rank_needs(self, params: _lib.Params, ranks: int, my_rank: int, n_clusters, records,
+                   flags_out_ptr: int) -> None:
+        """LET step one: per cluster of every owner's tree (owner order
+        0..R-1, device pointers), bit 0 = moment row needed, bit 1 =
+        particles needed, written as int32 to the device buffer flags_out."""
+        R = int(ranks)
+        nc = np.ascontiguousarray(n_clusters, dtype=np.int64)
+        rec = (ctypes.c_void_p * R)(*[ctypes.c_void_p(int(v)) for v in records])
+        _lib.check(self._lib.bltc_rank_needs(self.handle, ctypes.byref(params), R, int(my_rank),
+                                             _lib.i64p(nc), rec, ctypes.c_void_p(flags_out_ptr)))
+
     # -- stage exports of the last run (bit-exact structure checks) ------------
     def sizes(self) -> _lib.Sizes:
         sz = _lib.Sizes()

@@ -71,6 +71,35 @@ class OracleRankEngine:
         mrow = rec[:, 16].astype(np.int64)
         return t, rows, mrow
 
+    def needs(self, ranks, my_rank, records):
+        """LET step one: need flags per cluster of every owner's tree."""
+        c = self.cfg
+        out = []
+        for o in range(ranks):
+            rec = records[o].numpy()
+            t = self._tree_geometry(rec)
+            lists = orc.build_lists(self.batches, t, c.theta, c.degree)
+            f = np.zeros(rec.shape[0], dtype=np.int32)
+            f[np.unique(lists.a_idx)] |= 1
+            f[np.unique(lists.d_idx)] |= 2
+            out.append(torch.from_numpy(f))
+        return out
+
+    @staticmethod
+    def _tree_geometry(rec):
+        nc = rec.shape[0]
+        cs = rec[:, 11].astype(np.int64)
+        z = np.zeros(0)
+        # the MAC reads the record's count (field 10); particle ranges may have
+        # been remapped by the LET exchange
+        return orc.Tree(order=np.zeros(0, np.int64), perm=np.zeros(0, np.int64),
+                        start=np.zeros(nc, np.int64), stop=rec[:, 10].astype(np.int64),
+                        lo=rec[:, 0:3].copy(), hi=rec[:, 3:6].copy(),
+                        child_start=np.where(cs < 0, 0, cs),
+                        child_count=rec[:, 12].astype(np.int64), depth=np.zeros(nc, np.int32),
+                        leaf_dfs=np.zeros(0, np.int64), center=rec[:, 6:9].copy(),
+                        radius=rec[:, 9].copy(), x=z, y=z, z=z, q=z)
+
     def evaluate(self, ranks, my_rank, forest):
         c = self.cfg
         owners = [my_rank] + [o for o in range(ranks) if o != my_rank]
@@ -78,8 +107,9 @@ class OracleRankEngine:
         direct = approx = 0
         for o in owners:
             t, rows, mrow = self._tree_from(forest[o], c.degree)
-            lists = orc.build_lists(self.batches, t, c.theta, c.degree)
-            d, a = orc.count_pairs(lists, self.batches, t.count, c.degree)
+            tg = self._tree_geometry(forest[o].records.numpy())
+            lists = orc.build_lists(self.batches, tg, c.theta, c.degree)
+            d, a = orc.count_pairs(lists, self.batches, tg.count, c.degree)
             direct += d
             approx += a
             groups.append(orc.SourceGroup(t, rows, mrow, lists))

@@ -61,7 +61,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, case, out_dir):
+def _worker(rank, world, port, case, out_dir, exchange="replicate"):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -79,8 +79,12 @@ def _worker(rank, world, port, case, out_dir):
     kernel = [bltc.coulomb(), bltc.yukawa(float(g["kappa"]))][int(g["kind"])]
     cfg = bltc.EvalConfig(theta=float(g["theta"]), degree=int(g["degree"]),
                           leaf_size=int(g["leaf"]), batch_size=int(g["batch"]), kernel=kernel)
-    phi, st = run_distributed(s, cfg, ranks=world, engine_factory=lambda: OracleRankEngine(cfg))
+    phi, st = run_distributed(s, cfg, ranks=world, engine_factory=lambda: OracleRankEngine(cfg),
+                              exchange=exchange)
     np.save(os.path.join(out_dir, f"phi{rank}.npy"), phi)
+    fetch = [[o, w, f.tree_records, f.clusters, f.moments, f.particles]
+             for (o, w), f in sorted(st.fetch_stats.items())]
+    np.save(os.path.join(out_dir, f"fetch{rank}.npy"), np.array(fetch, dtype=np.int64))
     np.save(os.path.join(out_dir, f"pairs{rank}.npy"), np.array([st.direct_pairs,
                                                                  st.approx_pairs]))
     dist.destroy_process_group()
@@ -122,3 +126,54 @@ def test_single_process_orchestration_matches_oracle(oracle):
     assert st.approx_pairs == int(g["approx_pairs"])
     assert sorted(st.rank_counts.tolist()) == [2000] * 4
     assert set(st.fetch_stats) == {(o, w) for o in range(4) for w in range(4) if o != w}
+
+
+def test_gloo_world3_let_exchange_matches_reference(tmp_path):
+    """Three processes, the two-step LET exchange (records all-gather, need
+    flags, all-to-all of ids and of exactly the referenced moment rows and
+    particle slices): potentials bitwise the reference's run_distributed and
+    the fetch volume per (origin, owner) equal to the reference's LET."""
+    import torch.multiprocessing as mp
+    case = "dist_r3"
+    g = golden(case)
+    mp.start_processes(_worker, args=(3, _free_port(), case, str(tmp_path), "let"), nprocs=3,
+                       join=True, start_method="spawn")
+    for r in range(3):
+        np.testing.assert_array_equal(np.load(tmp_path / f"phi{r}.npy"), g["phi"])
+        mine = np.load(tmp_path / f"fetch{r}.npy")
+        np.testing.assert_array_equal(mine, g["fetch"][g["fetch"][:, 0] == r])
+
+
+def test_single_process_let_matches_reference_fetch():
+    """ranks=4 in one process with the LET exchange: potentials bitwise, fetch
+    statistics equal to the reference's, no sufficiency/minimality violation."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import paper_2003_01836_b200 as bltc
+    from paper_2003_01836_b200.decomp import let_local, let_violations, run_distributed
+    from rank_engine_oracle import OracleRankEngine
+    g = golden("dist_r4_yukawa")
+    s = golden_system(g)
+    cfg = bltc.EvalConfig(theta=0.7, degree=6, leaf_size=300, batch_size=300,
+                          kernel=bltc.yukawa(0.5))
+    phi, st = run_distributed(s, cfg, ranks=4, engine_factory=lambda: OracleRankEngine(cfg),
+                              exchange="let")
+    np.testing.assert_array_equal(phi, g["phi"])
+    fetch = np.array([[o, w, f.tree_records, f.clusters, f.moments, f.particles]
+                      for (o, w), f in sorted(st.fetch_stats.items())], dtype=np.int64)
+    np.testing.assert_array_equal(fetch, g["fetch"])
+    # violations of one origin's fetched forest
+    part = rcb_partition(s.sources, 4)
+    engines = {}
+    for r in range(4):
+        idx = part.rank_indices(r)
+        engines[r] = OracleRankEngine(cfg)
+        src = s.sources
+        engines[r].build(src.x[idx], src.y[idx], src.z[idx], s.charges[idx])
+    pubs = {r: engines[r].publish() for r in range(4)}
+    needs = {r: (lambda recs, r=r: engines[r].needs(4, r, recs)) for r in range(4)}
+    forests, _ = let_local(pubs, needs, 4)
+    recs = [pubs[r].records for r in range(4)]
+    for me in range(4):
+        v = let_violations(forests[me], engines[me].needs(4, me, recs), me)
+        assert v == {"sufficiency": 0, "minimality": 0}

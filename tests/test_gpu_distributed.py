@@ -70,3 +70,22 @@ def test_plummer_ranks_vs_oracle(bltc, oracle, ranks):
     assert (st.direct_pairs, st.approx_pairs) == (info["direct_pairs"], info["approx_pairs"])
     phi_f, _ = run_distributed(s, cfg, ranks=ranks, mode="fast")
     _check(phi_f, ref, False)
+
+
+@pytest.mark.parametrize("case", ["dist_r3", "dist_r4_yukawa"])
+def test_let_exchange_matches_reference_fetch(bltc, case):
+    """The two-step LET exchange on the device (bltc_rank_needs + the fetched,
+    remapped forest): potentials bitwise those of the replicated forest, fetch
+    volume per (origin, owner) equal to the reference's build_let."""
+    from paper_2003_01836_b200.decomp import run_distributed
+    g = golden(case)
+    s = golden_system(g)
+    R = int(g["ranks"])
+    phi_l, st_l = run_distributed(s, _cfg(bltc, g), ranks=R, mode="parity", exchange="let")
+    phi_r, st_r = run_distributed(s, _cfg(bltc, g), ranks=R, mode="parity",
+                                  exchange="replicate")
+    np.testing.assert_array_equal(phi_l, phi_r)
+    fetch = np.array([[o, w, f.tree_records, f.clusters, f.moments, f.particles]
+                      for (o, w), f in sorted(st_l.fetch_stats.items())], dtype=np.int64)
+    np.testing.assert_array_equal(fetch, g["fetch"])
+    assert (st_l.direct_pairs, st_l.approx_pairs) == (st_r.direct_pairs, st_r.approx_pairs)
