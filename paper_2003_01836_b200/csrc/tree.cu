@@ -95,6 +95,8 @@ __device__ __forceinline__ void box_flush(int nd, unsigned long long (&mn)[3],
 __global__ void k_box(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
                       const double* __restrict__ z, const int32_t* __restrict__ node_of,
                       unsigned long long* box_u) {
+  constexpr int kU = 4;                    // 32-particle groups loaded ahead
+  constexpr int kNone = -2147483647 - 1;   // past the chunk end
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t c0 = warp * kBoxChunk;
@@ -102,43 +104,52 @@ __global__ void k_box(int64_t n, const double* __restrict__ x, const double* __r
   const int64_t c1 = min(c0 + kBoxChunk, n);
   unsigned long long mn[3] = {~0ull, ~0ull, ~0ull}, mx[3] = {0ull, 0ull, 0ull};
   int cur = node_of[c0];   // warp-uniform: node being accumulated
-  for (int64_t base = c0; base < c1; base += 32) {
-    const int64_t i = base + lane;
-    const bool valid = i < c1;
-    const int nd = valid ? node_of[i] : cur;
-    unsigned long long v[3] = {0ull, 0ull, 0ull};
-    if (valid && nd >= 0) {
-      v[0] = d2ord(x[i]);
-      v[1] = d2ord(y[i]);
-      v[2] = d2ord(z[i]);
-    }
-    const bool mine = valid && nd == cur;
-    if (mine) {
+  for (int64_t base = c0; base < c1; base += 32 * kU) {
+    int ndu[kU];
+    unsigned long long vu[kU][3];
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        mn[d] = v[d] < mn[d] ? v[d] : mn[d];
-        mx[d] = v[d] > mx[d] ? v[d] : mx[d];
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = base + 32 * u + lane;
+      ndu[u] = i < c1 ? node_of[i] : kNone;
+      vu[u][0] = vu[u][1] = vu[u][2] = 0ull;
+      if (i < c1) {
+        vu[u][0] = d2ord(x[i]);
+        vu[u][1] = d2ord(y[i]);
+        vu[u][2] = d2ord(z[i]);
       }
     }
-    if (__all_sync(0xffffffffu, !valid || nd == cur)) continue;
-    // node boundary inside these 32 particles
-    box_flush(cur, mn, mx, box_u, lane);
-    const int last = __shfl_sync(0xffffffffu, nd, 31);   // invalid lanes hold cur
-    if (valid && nd >= 0 && nd != cur && nd != last) {   // nodes wholly inside: rare
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        atomicMin(&box_u[(int64_t)nd * 6 + d], v[d]);
-        atomicMax(&box_u[(int64_t)nd * 6 + 3 + d], v[d]);
-      }
-    }
-    if (valid && nd == last && last != cur) {
+    for (int u = 0; u < kU; ++u) {
+      const bool valid = ndu[u] != kNone;
+      const int nd = valid ? ndu[u] : cur;
+      const unsigned long long* v = vu[u];
+      if (valid && nd == cur) {
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        mn[d] = v[d];
-        mx[d] = v[d];
+        for (int d = 0; d < 3; ++d) {
+          mn[d] = v[d] < mn[d] ? v[d] : mn[d];
+          mx[d] = v[d] > mx[d] ? v[d] : mx[d];
+        }
       }
+      if (__all_sync(0xffffffffu, nd == cur)) continue;
+      // node boundary inside these 32 particles
+      box_flush(cur, mn, mx, box_u, lane);
+      const int last = __shfl_sync(0xffffffffu, nd, 31);   // invalid lanes hold cur
+      if (valid && nd >= 0 && nd != cur && nd != last) {   // nodes wholly inside: rare
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          atomicMin(&box_u[(int64_t)nd * 6 + d], v[d]);
+          atomicMax(&box_u[(int64_t)nd * 6 + 3 + d], v[d]);
+        }
+      }
+      if (valid && nd == last && last != cur) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          mn[d] = v[d];
+          mx[d] = v[d];
+        }
+      }
+      cur = last;
     }
-    cur = last;
   }
   box_flush(cur, mn, mx, box_u, lane);
 }
