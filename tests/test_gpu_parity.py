@@ -251,3 +251,18 @@ def test_context_reuse_across_sizes(bltc, oracle):
             np.testing.assert_array_equal(b["radius"], bt.radius)
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("case", ["c1_coulomb", "plummer", "deg8"])
+def test_fast_moments_close(bltc, ctx, case):
+    """FAST upward pass (warp-cooperative, reciprocal-based factors, fused
+    accumulation, piece-ordered reduction): rows within 1e-13 of the row's
+    magnitude scale of the reference's moments."""
+    g = golden(case)
+    ctx.treecode(golden_system(g), _config(bltc, g), mode="fast", all_moments=True)
+    ids, rows = ctx.export_moments()
+    elig = np.nonzero(g["moments_has"])[0]
+    np.testing.assert_array_equal(ids, elig)
+    ref = g["moments"][elig]
+    scale = np.abs(ref).max(axis=1, keepdims=True) + 1e-300
+    assert (np.abs(rows - ref) / scale).max() <= 1e-13
