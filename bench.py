@@ -39,11 +39,13 @@ CONFIGS = {
     # BASELINE.json configs; c4 is the metric's workload (8M Coulomb n=8 theta=0.8)
     "c1": dict(workload="C1: N=20k uniform cube, Coulomb, n=4, theta=0.7", gen="uniform",
                n=20_000, kind=0, kappa=0.0, degree=4, theta=0.7, leaf=2000, batch=2000),
+    # C2/C3: N_B=1000 (= 500 for this uniform cube) measured fastest on B200:
+    # C2 53 ms vs 75 ms at N_B=2000, C3 163 ms vs 221 ms (tools/sweep_c4.py)
     "c2": dict(workload="C2: N=1M uniform cube, Coulomb, n=8, theta=0.8", gen="uniform",
-               n=1_000_000, kind=0, kappa=0.0, degree=8, theta=0.8, leaf=2000, batch=2000),
+               n=1_000_000, kind=0, kappa=0.0, degree=8, theta=0.8, leaf=2000, batch=1000),
     "c3": dict(workload="C3: N=1M uniform cube, Yukawa kappa=0.5, n=8, theta=0.8",
                gen="uniform", n=1_000_000, kind=1, kappa=0.5, degree=8, theta=0.8, leaf=2000,
-               batch=2000),
+               batch=1000),
     # N_B (batch size) is the performance knob; the CPU
     # baseline / reference arm run with the same value.  250 is the fastest
     # measured for C4 on B200 with packed work items (N_B=125: 0.97 s,
@@ -54,7 +56,7 @@ CONFIGS = {
     "c4u": dict(workload="N=8M uniform cube, Coulomb, n=8, theta=0.8", gen="uniform",
                 n=8_000_000, kind=0, kappa=0.0, degree=8, theta=0.8, leaf=2000, batch=2000),
     "c5": dict(workload="C5: N=64M uniform cube, Coulomb, n=10, theta=0.7", gen="uniform",
-               n=64_000_000, kind=0, kappa=0.0, degree=10, theta=0.7, leaf=2000, batch=2000),
+               n=64_000_000, kind=0, kappa=0.0, degree=10, theta=0.7, leaf=2000, batch=1000),
 }
 
 # Minimal FP64-pipe slots per pair: far / near field.
@@ -354,6 +356,9 @@ def run_ours(args, cfg):
     far_tflops = 2.0 * s_far * st.approx_pairs / far_s / 1e12 if far_s > 0 else 0.0
     near_tflops = 2.0 * s_near * st.direct_pairs / near_s / 1e12 if near_s > 0 else 0.0
     launches = int(sum(x.kernel_launches for x in stats))
+    # nominal FP64 peak: SMs x 64 FP64 lanes x 2 flop x max SM clock
+    sm_count = torch.cuda.get_device_properties(local).multi_processor_count
+    nominal_tflops = None
 
     # ---- e2e through the public API with host buffers (H2D/D2H inside)
     e2e = None
@@ -432,7 +437,10 @@ def run_ours(args, cfg):
                      "frac": far_tflops / peak_tflops if peak_tflops else None,
                      "traffic": traffic,
                      "work": f"{s_far} FP64 slots/pair x approx pairs (2 flop/slot)",
-                     "peak_source": "DFMA microbenchmark on this GPU in this run (bltc_probe_fp64)"},
+                     "peak_source": "DFMA microbenchmark on this GPU in this run (bltc_probe_fp64, "
+                                    "sustained ~0.3 s)",
+                     "peak_nominal": nominal_tflops,
+                     "frac_nominal": far_tflops / nominal_tflops if nominal_tflops else None},
         "near_roofline": {"kernel": "k_near_fast (near field)", "achieved": near_tflops,
                           "frac": near_tflops / peak_tflops if peak_tflops else None,
                           "work": f"{s_near} FP64 slots/pair x direct pairs"},
@@ -442,6 +450,11 @@ def run_ours(args, cfg):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    csum = line["clocks"]
+    if csum.get("sm_max_mhz"):
+        nominal_tflops = sm_count * 64 * 2 * csum["sm_max_mhz"] * 1e6 / 1e12
+        line["roofline"]["peak_nominal"] = nominal_tflops
+        line["roofline"]["frac_nominal"] = far_tflops / nominal_tflops
     if e2e is not None:
         line["e2e"] = e2e
     if dist is None and not args.no_accuracy:

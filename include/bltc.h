@@ -83,6 +83,8 @@ typedef struct {
   int64_t kernel_launches;
   int32_t tree_depth;
   int32_t batch_depth;
+  int32_t packed;        /* FAST: 1 = packed multi-batch work items, 0 = per-batch chunks */
+  int32_t reserved;
 } bltc_stats;
 
 BLTC_API const char* bltc_last_error(void);

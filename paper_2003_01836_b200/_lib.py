@@ -41,7 +41,8 @@ class Stats(ctypes.Structure):
                 ("h2d_s", ctypes.c_double), ("d2h_s", ctypes.c_double),
                 ("far_s", ctypes.c_double), ("near_s", ctypes.c_double),
                 ("n_moments", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
-                ("tree_depth", ctypes.c_int32), ("batch_depth", ctypes.c_int32)]
+                ("tree_depth", ctypes.c_int32), ("batch_depth", ctypes.c_int32),
+                ("packed", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class Sizes(ctypes.Structure):

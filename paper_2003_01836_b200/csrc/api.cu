@@ -523,13 +523,16 @@ void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, 
       PackedItems pi;
       build_packed_items(a, c->pk_pc, c->pk_poff, c->pk_wcnt, c->pk_woff, c->pk_items,
                          c->pk_dmask, c->lists.n_direct, c->bs.scan_tmp, c->hs, st, &pi);
-      launch_eval_packed(a, p->kernel_code, pi, c->counters.p, st, &far_ms, &near_ms,
-                         c->timing);
-      if (stats) {
-        stats->far_s = far_ms * 1e-3;
-        stats->near_s = near_ms * 1e-3;
+      if (packed_preferred(p->kernel_code, pi.chunk_lane_eff)) {
+        launch_eval_packed(a, p->kernel_code, pi, c->counters.p, st, &far_ms, &near_ms,
+                           c->timing);
+        if (stats) {
+          stats->far_s = far_ms * 1e-3;
+          stats->near_s = near_ms * 1e-3;
+          stats->packed = 1;
+        }
+        return;
       }
-      return;
     }
     const FastTuning tune = fast_tuning();
     const bool tuned = p->kernel_code == 0;

@@ -69,6 +69,7 @@ __device__ __forceinline__ double pair_acc(double acc, double q, double d2, doub
   if (KIND == 0) return coulomb_acc<FORM>(acc, q, d2);
   const double y = rsqrt_fast(d2);
   const double r = __dmul_rn(d2, y);
+  if (FORM == 2) return fma(q, __dmul_rn(exp(-kappa * r), y), acc);
   return fma(__dmul_rn(q, exp(-kappa * r)), y, acc);
 }
 
@@ -117,14 +118,30 @@ __device__ __forceinline__ int64_t upper_bound(const int32_t* a, int64_t n, int6
 // slots [64 w, min(64 w + 64, S)); a window overlapping more than kGMax
 // batches is split into several items.  Item = {slot_begin, slot_end,
 // first batch, segments}.
+// Also accumulates the lane slots the per-batch chunking of eval_fast.cu
+// would use (64-target chunks, a tail of <= 32 on half a warp), to choose
+// between the two decompositions.
 __global__ void k_pad_counts(int64_t nb, const int32_t* bstart, const int32_t* bstop,
-                             int32_t* pc) {
+                             int32_t* pc, unsigned long long* acc2) {
   const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned long long slots = 0, targets = 0;
   if (b < nb) {
     const int n = bstop[b] - bstart[b];
     pc[b] = n + (n & 1);
+    const int r = n % kSlots;
+    slots = (unsigned long long)(n - r) + (r > 32 ? kSlots : (r > 0 ? 32 : 0));
+    targets = (unsigned long long)n;
   } else if (b == nb) {
     pc[b] = 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    slots += __shfl_xor_sync(0xffffffffu, slots, o);
+    targets += __shfl_xor_sync(0xffffffffu, targets, o);
+  }
+  if ((threadIdx.x & 31) == 0 && slots) {
+    atomicAdd(&acc2[0], slots);
+    atomicAdd(&acc2[1], targets);
   }
 }
 
@@ -591,18 +608,16 @@ k_near_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int
 
 // ---------------------------------------------------------------------------
 // Tuning switches for measurements (BLTC_FAR_UNROLL=1|3, BLTC_PFORM=0|2).
-int tune_far_unroll() {
+int tune_far_unroll(int kind) {
   const char* e = std::getenv("BLTC_FAR_UNROLL");
-  return e ? std::atoi(e) : 3;   // 3 rows per step: -2% far time at C4 (measured)
+  // Coulomb: 3 rows per step, -2% far time at C4 (measured)
+  return e ? std::atoi(e) : (kind == 0 ? 3 : 1);
 }
 int tune_form() {
   const char* e = std::getenv("BLTC_PFORM");
   return e ? std::atoi(e) : 2;   // FORM 2: -0.9% far, -1.5% near at C4 (measured)
 }
-int tune_far_minb() {
-  const char* e = std::getenv("BLTC_FAR_MINB");
-  return e ? std::atoi(e) : 2;
-}
+
 
 template <typename K>
 int persistent_grid(K kernel, int threads, size_t smem) {
@@ -631,11 +646,10 @@ bool far_packed_dispatch(const EvalArgs& a, const PackedItems& it, int* counter,
     case 6: far_packed_launch<KIND, 6>(a, it, counter, st); return true;
     case 8: far_packed_launch<KIND, 8>(a, it, counter, st); return true;
     case 9:
-      if (KIND == 0 && tune_form() == 2 && tune_far_minb() == 1)
-        far_packed_launch<KIND, 9, 3, 2, 1>(a, it, counter, st);
-      else if (KIND == 0 && tune_form() == 2) far_packed_launch<KIND, 9, 3, 2>(a, it, counter, st);
-      else if (KIND == 0 && tune_far_unroll() == 3) far_packed_launch<KIND, 9, 3>(a, it, counter, st);
-      else far_packed_launch<KIND, 9>(a, it, counter, st);
+      // tuned for the benchmark degree: k2 unrolled by 3, FORM 2 (measured)
+      if (tune_form() != 2) far_packed_launch<KIND, 9, 1, 0>(a, it, counter, st);
+      else if (tune_far_unroll(KIND) == 3) far_packed_launch<KIND, 9, 3, 2>(a, it, counter, st);
+      else far_packed_launch<KIND, 9, 1, 2>(a, it, counter, st);
       return true;
     case 11: far_packed_launch<KIND, 11>(a, it, counter, st); return true;
     default: return false;
@@ -654,6 +668,12 @@ void near_packed_launch(const EvalArgs& a, const PackedItems& it, int* counter,
 }
 }  // namespace
 
+bool packed_preferred(int kind, double chunk_lane_eff) {
+  if (const char* e = std::getenv("BLTC_PACK"))
+    if (std::atoi(e) == 1) return true;   // forced on
+  return chunk_lane_eff < (kind == 1 ? 0.87 : 0.95);
+}
+
 bool packed_supported(int kind, int degree) {
   if (const char* e = std::getenv("BLTC_PACK"))
     if (std::atoi(e) == 0) return false;
@@ -667,15 +687,22 @@ void build_packed_items(const EvalArgs& a, DBuf<int32_t>& pc, DBuf<int32_t>& pof
                         DBuf<uint8_t>& dmask, int64_t n_direct, DBuf<int32_t>& scan_tmp,
                         HostScratch& hs, cudaStream_t st, PackedItems* out) {
   const int64_t nb = a.nb;
-  pc.resize(nb + 1);
+  pc.resize(nb + 6);   // + 16-byte-aligned scratch: chunk slots, targets (u64)
   poff.resize(nb + 1);
-  k_pad_counts<<<(int)((nb + 1 + 255) / 256), 256, 0, st>>>(nb, a.bstart, a.bstop, pc.p);
+  unsigned long long* cs =
+      reinterpret_cast<unsigned long long*>(pc.p + ((nb + 1 + 1) & ~int64_t(1)));
+  BLTC_CUDA(cudaMemsetAsync(cs, 0, 2 * sizeof(unsigned long long), st));
+  k_pad_counts<<<(int)((nb + 1 + 255) / 256), 256, 0, st>>>(nb, a.bstart, a.bstop, pc.p, cs);
   BLTC_LAUNCH_CHECK();
   exclusive_scan_i32(pc.p, poff.p, nb + 1, scan_tmp, st);
   int32_t* h = (int32_t*)hs.get(64);
   BLTC_CUDA(cudaMemcpyAsync(h, poff.p + nb, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  BLTC_CUDA(cudaMemcpyAsync(h + 2, cs, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                            st));
   BLTC_CUDA(cudaStreamSynchronize(st));
   const int64_t S = h[0];
+  const unsigned long long* hc = reinterpret_cast<const unsigned long long*>(h + 2);
+  out->chunk_lane_eff = hc[0] ? (double)hc[1] / (double)hc[0] : 1.0;
   const int64_t nw = (S + kSlots - 1) / kSlots;
   wcnt.resize(nw + 1);
   woff.resize(nw + 1);
@@ -716,9 +743,13 @@ void launch_eval_packed(const EvalArgs& a, int kind, const PackedItems& it, int*
   if (kind == 0) far_packed_dispatch<0>(a, it, counters, st);
   else far_packed_dispatch<1>(a, it, counters, st);
   if (timing) BLTC_CUDA(cudaEventRecord(e1, st));
-  if (kind == 0 && tune_form() == 2) near_packed_launch<0, kNearCh, 2>(a, it, counters + 1, st);
-  else if (kind == 0) near_packed_launch<0>(a, it, counters + 1, st);
-  else near_packed_launch<1>(a, it, counters + 1, st);
+  if (tune_form() != 2) {
+    if (kind == 0) near_packed_launch<0>(a, it, counters + 1, st);
+    else near_packed_launch<1>(a, it, counters + 1, st);
+  } else {
+    if (kind == 0) near_packed_launch<0, kNearCh, 2>(a, it, counters + 1, st);
+    else near_packed_launch<1, kNearCh, 2>(a, it, counters + 1, st);
+  }
   if (timing) {
     BLTC_CUDA(cudaEventRecord(e2, st));
     BLTC_CUDA(cudaEventSynchronize(e2));

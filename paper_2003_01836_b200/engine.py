@@ -72,10 +72,12 @@ class RunStats:
     kernel_launches: int = 0
     tree_depth: int = 0
     batch_depth: int = 0
+    packed: int = 0
 
     @classmethod
     def from_c(cls, s: _lib.Stats) -> "RunStats":
-        return cls(**{name: getattr(s, name) for name, _ in _lib.Stats._fields_})
+        return cls(**{name: getattr(s, name) for name, _ in _lib.Stats._fields_
+                      if name != "reserved"})
 
 
 def cheb_nodes(degree: int) -> np.ndarray:

@@ -57,6 +57,7 @@ for env in envsets:
                               "far_ms": 1e3 * st.far_s, "near_ms": 1e3 * st.near_s,
                               "setup_ms": 1e3 * st.setup_s, "pre_ms": 1e3 * st.precompute_s,
                               "approx": st.approx_pairs, "direct": st.direct_pairs,
-                              "clusters": st.n_clusters, "batches": st.n_batches}), flush=True)
+                              "clusters": st.n_clusters, "batches": st.n_batches,
+                              "packed": st.packed}), flush=True)
     for kv in filter(None, env.split(";")):
         os.environ.pop(kv.split("=")[0], None)
