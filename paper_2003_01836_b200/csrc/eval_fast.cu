@@ -89,7 +89,7 @@ __device__ __forceinline__ double pair_acc(double acc, double q, double d2, doub
   if (KIND == 1) {
     const double y = rsqrt_fast(d2);
     const double r = __dmul_rn(d2, y);
-    return fma(__dmul_rn(q, exp(-kappa * r)), y, acc);
+    return fma(__dmul_rn(q, exp_neg_fast(-__dmul_rn(kappa, r))), y, acc);
   }
   return __dadd_rn(acc, q);
 }
@@ -276,11 +276,14 @@ __device__ __forceinline__ void near_chunk(double (&part)[kTpt], const double4* 
       const double dx = __dsub_rn(tx[k], s.x);
       const double dy = __dsub_rn(ty[k], s.y);
       const double dz = __dsub_rn(tz[k], s.z);
-      const double d2 = fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx)));
       if (MASKED) {
+        // d2 + 1e-300: exactly d2 for every non-singular pair, never 0, so
+        // only the charge needs the select (excluded pairs add 0 * finite)
+        const double d2 = fma(dz, dz, fma(dy, dy, fma(dx, dx, 1e-300)));
         const bool ok = __double_as_longlong(d2) >= tb;
-        part[k] = pair_acc<KIND, FORM>(part[k], ok ? s.w : 0.0, ok ? d2 : 1.0, kappa);
+        part[k] = pair_acc<KIND, FORM>(part[k], ok ? s.w : 0.0, d2, kappa);
       } else {
+        const double d2 = fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx)));
         part[k] = pair_acc<KIND, FORM>(part[k], s.w, d2, kappa);
       }
     }

@@ -69,8 +69,9 @@ __device__ __forceinline__ double pair_acc(double acc, double q, double d2, doub
   if (KIND == 0) return coulomb_acc<FORM>(acc, q, d2);
   const double y = rsqrt_fast(d2);
   const double r = __dmul_rn(d2, y);
-  if (FORM == 2) return fma(q, __dmul_rn(exp(-kappa * r), y), acc);
-  return fma(__dmul_rn(q, exp(-kappa * r)), y, acc);
+  const double ex = exp_neg_fast(-__dmul_rn(kappa, r));
+  if (FORM == 2) return fma(q, __dmul_rn(ex, y), acc);
+  return fma(__dmul_rn(q, ex), y, acc);
 }
 
 __device__ __forceinline__ void neumaier(double& acc, double& comp, double t) {
@@ -413,11 +414,14 @@ __device__ __forceinline__ void near_chunk(double (&part)[2], const double4* src
       const double dx = __dsub_rn(tx[t], s.x);
       const double dy = __dsub_rn(ty[t], s.y);
       const double dz = __dsub_rn(tz[t], s.z);
-      const double d2 = fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx)));
       if (MASKED) {
+        // d2 + 1e-300: exactly d2 for every non-singular pair, never 0, so
+        // only the charge needs the select (excluded pairs add 0 * finite)
+        const double d2 = fma(dz, dz, fma(dy, dy, fma(dx, dx, 1e-300)));
         const bool ok = __double_as_longlong(d2) >= tb;
-        part[t] = pair_acc<KIND, FORM>(part[t], ok ? s.w : 0.0, ok ? d2 : 1.0, kappa);
+        part[t] = pair_acc<KIND, FORM>(part[t], ok ? s.w : 0.0, d2, kappa);
       } else {
+        const double d2 = fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx)));
         part[t] = pair_acc<KIND, FORM>(part[t], s.w, d2, kappa);
       }
     }
@@ -671,7 +675,8 @@ void near_packed_launch(const EvalArgs& a, const PackedItems& it, int* counter,
 bool packed_preferred(int kind, double chunk_lane_eff) {
   if (const char* e = std::getenv("BLTC_PACK"))
     if (std::atoi(e) == 1) return true;   // forced on
-  return chunk_lane_eff < (kind == 1 ? 0.87 : 0.95);
+  (void)kind;
+  return chunk_lane_eff < 0.95;
 }
 
 bool packed_supported(int kind, int degree) {
