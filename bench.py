@@ -47,12 +47,13 @@ CONFIGS = {
                gen="uniform", n=1_000_000, kind=1, kappa=0.5, degree=8, theta=0.8, leaf=2000,
                batch=1000),
     # N_B (batch size) is the performance knob; the CPU
-    # baseline / reference arm run with the same value.  250 is the fastest
-    # measured for C4 on B200 with packed work items (N_B=125: 0.97 s,
-    # 250: 0.965 s, 500: 1.02 s, 1000: 1.11 s; tools/sweep_c4.py).
+    # baseline / reference arm run with the same value.  160 is the fastest
+    # measured for C4 on B200 with packed work items (N_B=125: 0.929 s,
+    # 160: 0.908 s, 250: 0.927 s, 400: 0.960 s; N_L 1000-3000 within 0.5%;
+    # tools/sweep_c4.py, gpurun_out/sweep27/28).
     "c4": dict(workload="C4: N=8M Plummer (a=1, r<=10a), Coulomb, n=8, theta=0.8",
                gen="plummer", n=8_000_000, kind=0, kappa=0.0, degree=8, theta=0.8, leaf=2000,
-               batch=250),
+               batch=160),
     "c4u": dict(workload="N=8M uniform cube, Coulomb, n=8, theta=0.8", gen="uniform",
                 n=8_000_000, kind=0, kappa=0.0, degree=8, theta=0.8, leaf=2000, batch=2000),
     "c5": dict(workload="C5: N=64M uniform cube, Coulomb, n=10, theta=0.7", gen="uniform",
