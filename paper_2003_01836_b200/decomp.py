@@ -206,6 +206,52 @@ def all_gather_records(pub: Published, ranks: int, group=None) -> list:
             for r in range(ranks)]
 
 
+@dataclass(eq=False)
+class LetPlan:
+    """What one origin fetches from every owner (build_let, decomp.py:366-399):
+    per owner the sorted moment-row ids ``a[o]`` and particle-slice ids
+    ``d[o]`` (device tensors) and, on the host, their counts, the number of
+    clusters in both lists and the particle count of the slices."""
+
+    a: dict
+    d: dict
+    na: dict
+    nd: dict
+    nboth: dict
+    npart: dict
+
+
+def let_plan(flags: list, records: list, me: int) -> LetPlan:
+    """All owners at once with three host synchronisations (not one per
+    owner and list): need flags -> ids, counts and particle totals."""
+    import torch
+    R = len(flags)
+    dev = flags[0].device
+    sizes = [int(f.numel()) for f in flags]
+    flat = torch.cat([f.to(torch.int64) for f in flags])
+    owner = torch.repeat_interleave(torch.arange(R, device=dev),
+                                    torch.tensor(sizes, device=dev))
+    offs = torch.tensor([0] + sizes[:-1], device=dev).cumsum(0)
+    local = torch.arange(flat.numel(), device=dev) - offs[owner]
+    remote = owner != me
+    a_pos = torch.nonzero(((flat & 1) != 0) & remote).reshape(-1)
+    d_pos = torch.nonzero(((flat & 2) != 0) & remote).reshape(-1)
+    # particle counts of the direct clusters, from the owners' records
+    cnt = torch.cat([r[:, 15] - r[:, 14] for r in records]).to(torch.int64)
+    both = ((flat & 3) == 3) & remote
+    stats = torch.stack([torch.bincount(owner[a_pos], minlength=R),
+                         torch.bincount(owner[d_pos], minlength=R),
+                         torch.bincount(owner[both], minlength=R),
+                         torch.bincount(owner[d_pos], weights=cnt[d_pos].to(torch.float64),
+                                        minlength=R).to(torch.int64)]).cpu()
+    na, nd, nb, npart = (stats[i].tolist() for i in range(4))
+    a_ids = torch.split(local[a_pos], na)
+    d_ids = torch.split(local[d_pos], nd)
+    return LetPlan(a={o: a_ids[o] for o in range(R)}, d={o: d_ids[o] for o in range(R)},
+                   na=dict(enumerate(na)), nd=dict(enumerate(nd)), nboth=dict(enumerate(nb)),
+                   npart=dict(enumerate(npart)))
+
+
 def let_request(flags) -> tuple:
     """Cluster ids one origin needs from one owner, each sorted ascending as
     in build_let (decomp.py:372-373): (moment-row ids, particle-slice ids)."""
@@ -216,31 +262,48 @@ def let_request(flags) -> tuple:
     return a, d
 
 
-def _slice_index(records, d_ids):
-    """Concatenated particle indices of the clusters d_ids (list order)."""
+def _slice_index(records, d_ids, total: int | None = None):
+    """Concatenated particle indices of the clusters d_ids (list order) and
+    the slice sizes; ``total`` (the sum of the sizes) avoids a host sync."""
     import torch
     dev = records.device
     if d_ids.numel() == 0:
-        return torch.zeros(0, dtype=torch.int64, device=dev), torch.zeros(0, dtype=torch.int64,
-                                                                          device=dev)
+        z = torch.zeros(0, dtype=torch.int64, device=dev)
+        return z, z
     st = records[d_ids, 14].to(torch.int64)
     sz = records[d_ids, 15].to(torch.int64) - st
     off = torch.cumsum(sz, 0) - sz
-    total = int(sz.sum().item())
-    seg = torch.repeat_interleave(torch.arange(d_ids.numel(), device=dev), sz)
+    if total is None:
+        total = int(sz.sum().item())
+    seg = torch.repeat_interleave(torch.arange(d_ids.numel(), device=dev), sz,
+                                  output_size=total)
     idx = st[seg] + (torch.arange(total, device=dev) - off[seg])
     return idx, sz
 
 
-def let_serve(pub: Published, a_ids, d_ids):
+def let_serve(pub: Published, a_ids, d_ids, npart: int | None = None):
     """Owner side of step two: the requested moment rows and particle slices,
     flattened into one float64 buffer (rows first)."""
     import torch
     mrow = pub.records[a_ids, 16].to(torch.int64)
     rows = pub.moments[mrow] if a_ids.numel() else pub.moments[:0]
-    idx, _ = _slice_index(pub.records, d_ids)
+    idx, _ = _slice_index(pub.records, d_ids, npart)
     par = pub.particles[:, idx]
     return torch.cat([rows.reshape(-1), par.reshape(-1)])
+
+
+def let_serve_many(pub: Published, requests: list):
+    """let_serve for several requesters [(a_ids, d_ids) | None] with one host
+    synchronisation for all their particle totals."""
+    import torch
+    live = [i for i, r in enumerate(requests) if r is not None and r[1].numel()]
+    totals = {}
+    if live:
+        sums = torch.stack([(pub.records[requests[i][1], 15]
+                             - pub.records[requests[i][1], 14]).sum() for i in live]).cpu()
+        totals = {i: int(v) for i, v in zip(live, sums.tolist())}
+    return [None if r is None else let_serve(pub, r[0], r[1], totals.get(i, 0))
+            for i, r in enumerate(requests)]
 
 
 def let_payload_size(records, a_ids, d_ids, ncols: int) -> int:
@@ -251,7 +314,8 @@ def let_payload_size(records, a_ids, d_ids, ncols: int) -> int:
     return int(a_ids.numel()) * ncols + 4 * p
 
 
-def let_assemble(records, a_ids, d_ids, payload, ncols: int):
+def let_assemble(records, a_ids, d_ids, payload, ncols: int, npart: int | None = None,
+                 nboth: int | None = None):
     """Origin side of step two: the owner's fetched data as a Published whose
     records point into the fetched buffers (moment row -> index among the
     fetched rows, particle range -> offset in the fetched slices; records of
@@ -259,8 +323,8 @@ def let_assemble(records, a_ids, d_ids, payload, ncols: int):
     import torch
     na = int(a_ids.numel())
     rows = payload[:na * ncols].view(na, ncols)
-    _, sz = _slice_index(records, d_ids)
-    P = int(sz.sum().item()) if sz.numel() else 0
+    sz = (records[d_ids, 15] - records[d_ids, 14]).to(torch.int64)
+    P = int(sz.sum().item()) if npart is None else int(npart)
     par = payload[na * ncols:na * ncols + 4 * P].view(4, P)
     rec = records.clone()
     rec[:, 14] = 0.0
@@ -272,9 +336,11 @@ def let_assemble(records, a_ids, d_ids, payload, ncols: int):
         off = torch.cumsum(sz, 0) - sz
         rec[d_ids, 14] = off.to(rec.dtype)
         rec[d_ids, 15] = (off + sz).to(rec.dtype)
-    both = torch.unique(torch.cat([a_ids, d_ids]))
-    fs = FetchStats(tree_records=int(records.shape[0]), clusters=int(both.numel()),
-                    moments=na, particles=P)
+    if nboth is None:
+        nboth = int(a_ids.numel() + d_ids.numel()
+                    - torch.unique(torch.cat([a_ids, d_ids])).numel())
+    fs = FetchStats(tree_records=int(records.shape[0]),
+                    clusters=na + int(d_ids.numel()) - int(nboth), moments=na, particles=P)
     return Published(rec, par, rows), fs
 
 
@@ -288,34 +354,30 @@ def let_exchange(pub: Published, needs_fn, ranks: int, me: int, group=None):
     dev = pub.records.device
     ncols = int(pub.moments.shape[1])
     records = all_gather_records(pub, ranks, group)
-    flags = needs_fn(records)
-    req = {o: let_request(flags[o]) for o in range(ranks) if o != me}
+    plan = let_plan(needs_fn(records), records, me)
     # requests: counts, then ids
-    cnt = torch.zeros((ranks, 2), dtype=torch.int64, device=dev)
-    for o, (a, d) in req.items():
-        cnt[o, 0], cnt[o, 1] = a.numel(), d.numel()
+    cnt = torch.tensor([[plan.na[o], plan.nd[o]] if o != me else [0, 0] for o in range(ranks)],
+                       dtype=torch.int64, device=dev)
     rcnt = torch.empty_like(cnt)
     dist.all_to_all_single(rcnt, cnt, group=group)
-    send_ids = torch.cat([torch.cat(req[o]) if o in req else
-                          torch.zeros(0, dtype=torch.int64, device=dev) for o in range(ranks)])
-    in_split = [int(cnt[o].sum().item()) for o in range(ranks)]
-    out_split = [int(rcnt[o].sum().item()) for o in range(ranks)]
+    rcnt_h = rcnt.cpu().tolist()
+    send_ids = torch.cat([torch.cat([plan.a[o], plan.d[o]]) for o in range(ranks)])
+    in_split = [plan.na[o] + plan.nd[o] if o != me else 0 for o in range(ranks)]
+    out_split = [sum(c) for c in rcnt_h]
     recv_ids = torch.empty(sum(out_split), dtype=torch.int64, device=dev)
     dist.all_to_all_single(recv_ids, send_ids, out_split, in_split, group=group)
     # serve every requester
-    parts, serve_split, pos = [], [], 0
+    reqs, pos = [], 0
     for r in range(ranks):
-        na, nd = int(rcnt[r, 0].item()), int(rcnt[r, 1].item())
+        na, nd = rcnt_h[r]
         ids = recv_ids[pos:pos + na + nd]
         pos += na + nd
-        if r == me or na + nd == 0:
-            serve_split.append(0)
-            continue
-        buf = let_serve(pub, ids[:na], ids[na:])
-        parts.append(buf)
-        serve_split.append(int(buf.numel()))
-    send = torch.cat(parts) if parts else torch.zeros(0, dtype=torch.float64, device=dev)
-    fetch_split = [let_payload_size(records[o], *req[o], ncols) if o in req else 0
+        reqs.append(None if (r == me or na + nd == 0) else (ids[:na], ids[na:]))
+    bufs = let_serve_many(pub, reqs)
+    serve_split = [0 if b is None else int(b.numel()) for b in bufs]
+    live = [b for b in bufs if b is not None]
+    send = torch.cat(live) if live else torch.zeros(0, dtype=torch.float64, device=dev)
+    fetch_split = [plan.na[o] * ncols + 4 * plan.npart[o] if o != me else 0
                    for o in range(ranks)]
     recv = torch.empty(sum(fetch_split), dtype=torch.float64, device=dev)
     dist.all_to_all_single(recv, send, fetch_split, serve_split, group=group)
@@ -326,7 +388,8 @@ def let_exchange(pub: Published, needs_fn, ranks: int, me: int, group=None):
             continue
         payload = recv[pos:pos + fetch_split[o]]
         pos += fetch_split[o]
-        p_o, fs = let_assemble(records[o], *req[o], payload, ncols)
+        p_o, fs = let_assemble(records[o], plan.a[o], plan.d[o], payload, ncols,
+                               plan.npart[o], plan.nboth[o])
         forest.append(p_o)
         fetch[(me, o)] = fs
     return forest, fetch
@@ -334,20 +397,20 @@ def let_exchange(pub: Published, needs_fn, ranks: int, me: int, group=None):
 
 def let_local(pubs: dict, needs_fns: dict, ranks: int):
     """Both LET steps for ranks simulated in one process (no process group):
-    the same request / serve / assemble path, handed over in place."""
+    the same plan / serve / assemble path, handed over in place."""
     ncols = int(pubs[0].moments.shape[1])
     records = [pubs[r].records for r in range(ranks)]
     forests, fetch = {}, {}
     for me in range(ranks):
-        flags = needs_fns[me](records)
+        plan = let_plan(needs_fns[me](records), records, me)
         forest = []
         for o in range(ranks):
             if o == me:
                 forest.append(pubs[me])
                 continue
-            a, d = let_request(flags[o])
-            payload = let_serve(pubs[o], a, d)
-            p_o, fs = let_assemble(records[o], a, d, payload, ncols)
+            payload = let_serve(pubs[o], plan.a[o], plan.d[o], plan.npart[o])
+            p_o, fs = let_assemble(records[o], plan.a[o], plan.d[o], payload, ncols,
+                                   plan.npart[o], plan.nboth[o])
             forest.append(p_o)
             fetch[(me, o)] = fs
         forests[me] = forest
