@@ -142,6 +142,15 @@ def eval_config(cfg: dict, batch: int | None, leaf: int | None):
                       kernel=kernel)
 
 
+def launch_count() -> int:
+    """libbltc's process-wide kernel launch counter (bltc_launch_count)."""
+    import ctypes
+    from paper_2003_01836_b200 import _lib
+    v = ctypes.c_int64()
+    _lib.check(_lib.load().bltc_launch_count(ctypes.byref(v)))
+    return int(v.value)
+
+
 def probe_fp64(device: int) -> float:
     import ctypes
     from paper_2003_01836_b200 import _lib
@@ -299,6 +308,8 @@ def run_ours(args, cfg):
     torch.cuda.set_device(local)
     dist = None
     if world > 1 or args.rank_path:
+        # keep stdout to the one JSON line (NCCL prints its version at INFO)
+        os.environ.setdefault("NCCL_DEBUG", "WARN")
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     econf = eval_config(cfg, args.batch_size, args.leaf_size)
@@ -341,11 +352,13 @@ def run_ours(args, cfg):
     e1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
+        l0 = launch_count()
         e0.record(stream)
         for _ in range(args.steps):
             stats.append(step())
         e1.record(stream)
         barrier()
+        l1 = launch_count()
     ms = e0.elapsed_time(e1) / args.steps
     if dist is not None:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -359,7 +372,7 @@ def run_ours(args, cfg):
     s_far, s_near = SLOTS[cfg["kind"]]
     far_tflops = 2.0 * s_far * st.approx_pairs / far_s / 1e12 if far_s > 0 else 0.0
     near_tflops = 2.0 * s_near * st.direct_pairs / near_s / 1e12 if near_s > 0 else 0.0
-    launches = int(sum(x.kernel_launches for x in stats))
+    launches = l1 - l0   # every libbltc kernel launched in the timed region
     # nominal FP64 peak: SMs x 64 FP64 lanes x 2 flop x max SM clock
     sm_count = torch.cuda.get_device_properties(local).multi_processor_count
     nominal_tflops = None

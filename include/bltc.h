@@ -202,6 +202,9 @@ BLTC_API int bltc_direct_sum(bltc_ctx* ctx, int32_t kernel_code, double kappa, i
  * Sustained FP64 FMA throughput of the device (DFMA/s), measured for about
  * `seconds`: the denominator of the FP64 roofline fraction bench.py reports. */
 BLTC_API int bltc_probe_fp64(int device, double seconds, double* dfma_per_s);
+/* Kernels libbltc has launched in this process so far (all contexts): the
+ * benchmark's count of its own launches inside a timed region. */
+BLTC_API int bltc_launch_count(int64_t* out);
 
 #ifdef __cplusplus
 }

@@ -90,6 +90,7 @@ SIGNATURES = {
     "bltc_rank_needs": (ctypes.c_int, [_vp, ctypes.POINTER(Params), ctypes.c_int32,
                                        ctypes.c_int32, _i64p, ctypes.POINTER(_vp), _vp]),
     "bltc_probe_fp64": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _f64p]),
+    "bltc_launch_count": (ctypes.c_int, [_i64p]),
     "bltc_direct_sum": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_double, ctypes.c_int32,
                                        ctypes.c_int64, _i64p, ctypes.c_int64, _f64p, _f64p,
                                        _f64p, ctypes.c_int64, _f64p, _f64p, _f64p, _f64p,

@@ -63,3 +63,9 @@ extern "C" BLTC_API int bltc_probe_fp64(int device, double seconds, double* dfma
     return BLTC_ERR_CUDA;
   }
 }
+
+extern "C" BLTC_API int bltc_launch_count(int64_t* out) {
+  if (!out) return BLTC_ERR_VALUE;
+  *out = (int64_t)bltc::g_launch_count;
+  return BLTC_OK;
+}
