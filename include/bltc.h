@@ -142,6 +142,52 @@ BLTC_API int bltc_export_lists(bltc_ctx* ctx, int64_t* a_ptr, int64_t* a_idx, in
 /* Moments: cluster ids [n_moments] and rows [n_moments][(n+1)^3]. */
 BLTC_API int bltc_export_moments(bltc_ctx* ctx, int64_t* cluster_ids, double* rows);
 
+/* ---- Stage calls with host-provided upstream structures -------------------
+ * Each stage of the pipeline on structures the caller built (e.g. the
+ * reference's own tree / batches / lists / moments, flattened), so a stage
+ * can be swapped in alone and checked bit for bit.  Trees are BFS cluster
+ * arrays as bltc_export_tree returns them (start/stop into the reordered
+ * particles, lo/hi [n][3], child_start/child_count), batches as
+ * bltc_export_batches.  Host pointers.
+ *
+ * bltc_stage_lists: build_interaction_lists (engine.py:128-130) of the batches
+ * against the tree; the lists stay in the context -- read them with
+ * bltc_export_lists (sizes in *n_approx / *n_direct). */
+BLTC_API int bltc_stage_lists(bltc_ctx* ctx, const bltc_params* p, int64_t n_batches,
+                              const int64_t* batch_start, const int64_t* batch_stop,
+                              const double* batch_center, const double* batch_radius,
+                              int64_t n_clusters, const int64_t* start, const int64_t* stop,
+                              const double* lo, const double* hi, const int64_t* child_start,
+                              const int64_t* child_count, int64_t* n_approx, int64_t* n_direct);
+/* bltc_stage_moments: compute_modified_charges (moments.py:132-144) of the
+ * clusters cluster_ids[0..n_list) of a tree whose sources (x, y, z, q) are in
+ * cluster order; rows_out [n_list][(n+1)^3], k1-major. */
+BLTC_API int bltc_stage_moments(bltc_ctx* ctx, const bltc_params* p, const double* cheb_s,
+                                int64_t n_s, const double* sx, const double* sy,
+                                const double* sz, const double* q, int64_t n_clusters,
+                                const int64_t* start, const int64_t* stop, const double* lo,
+                                const double* hi, int64_t n_list, const int64_t* cluster_ids,
+                                double* rows_out);
+/* bltc_stage_potentials: compute_potentials (engine.py:315-335).  Targets in
+ * batch order, sources in cluster order; lists as CSR over batches (entries:
+ * cluster ids); moment_row[c] = row of cluster c in rows ([n_rows][(n+1)^3]),
+ * -1 if none (every approximated cluster needs one).  perm (original index ->
+ * batch-order position) gives phi in the original order, NULL keeps batch
+ * order. */
+BLTC_API int bltc_stage_potentials(bltc_ctx* ctx, const bltc_params* p, const double* cheb_s,
+                                   int64_t n_t, const double* tx, const double* ty,
+                                   const double* tz, int64_t n_batches,
+                                   const int64_t* batch_start, const int64_t* batch_stop,
+                                   const double* batch_center, const double* batch_radius,
+                                   int64_t n_s, const double* sx, const double* sy,
+                                   const double* sz, const double* q, int64_t n_clusters,
+                                   const int64_t* start, const int64_t* stop, const double* lo,
+                                   const double* hi, const int64_t* a_ptr, const int64_t* a_idx,
+                                   const int64_t* d_ptr, const int64_t* d_idx,
+                                   const int64_t* moment_row, int64_t n_rows,
+                                   const double* rows, const int64_t* perm, double* phi_out,
+                                   bltc_stats* stats);
+
 /* ---- Distributed (one rank per GPU; decomp.py:483-593) ------------------
  * Each rank: bltc_rank_build (local tree, batches, moments of every cluster
  * that may be approximated) -> bltc_rank_publish_sizes / bltc_rank_publish

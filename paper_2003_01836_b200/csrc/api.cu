@@ -250,6 +250,7 @@ struct bltc_ctx {
   DBuf<int64_t> widen;
   bltc_params params{};
   bool have_run = false;
+  bool lists_staged = false;   // bltc_stage_lists result (exportable lists)
   int64_t launches = 0;
   // distributed: per-rank forest
   bool rank_built = false;
@@ -591,6 +592,7 @@ void run_pipeline(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64
   cudaStream_t st = c->st;
   c->params = *p;
   c->have_run = false;
+  c->lists_staged = false;
   const long long launches0 = g_launch_count;
   Timer tm(c->timing, st);
   upload_nodes(c, p, cheb_s);
@@ -686,9 +688,77 @@ void d2h_widen(bltc_ctx* c, int64_t* host, const int32_t* dev, int64_t n) {
   BLTC_CUDA(cudaStreamSynchronize(c->st));
 }
 
+
+// ---- host-structure stage calls: upload helpers ---------------------------
+template <typename T>
+void h2d(DBuf<T>& dst, const T* src, int64_t n, cudaStream_t st) {
+  dst.resize(n > 0 ? n : 1);
+  if (n > 0) BLTC_CUDA(cudaMemcpyAsync(dst.p, src, n * sizeof(T), cudaMemcpyHostToDevice, st));
+}
+
+// int64 host indices -> int32 device buffer (values must fit, checked)
+void h2d_narrow(DBuf<int32_t>& dst, const int64_t* src, int64_t n, cudaStream_t st,
+                const char* what) {
+  std::vector<int32_t> tmp(n > 0 ? n : 1);
+  for (int64_t i = 0; i < n; ++i) {
+    if (src[i] < INT32_MIN || src[i] > INT32_MAX) {
+      set_error(std::string(what) + " value out of the supported int32 range");
+      throw UserError{BLTC_ERR_UNSUPPORTED};
+    }
+    tmp[i] = (int32_t)src[i];
+  }
+  dst.resize(n > 0 ? n : 1);
+  if (n > 0) {
+    BLTC_CUDA(cudaMemcpyAsync(dst.p, tmp.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice,
+                              st));
+    BLTC_CUDA(cudaStreamSynchronize(st));   // tmp goes out of scope
+  }
+}
+
+void require_ptr(const void* ptr, const char* what) {
+  if (!ptr) {
+    set_error(std::string(what) + " is NULL");
+    throw UserError{BLTC_ERR_VALUE};
+  }
+}
+
+// Upload a source tree given as BFS arrays (tree.py:198-217 / bltc_export_tree)
+// into c->src and derive the MAC / evaluation records.
+void upload_tree(bltc_ctx* c, int64_t nc, const int64_t* start, const int64_t* stop,
+                 const double* lo, const double* hi, const int64_t* child_start,
+                 const int64_t* child_count) {
+  cudaStream_t st = c->st;
+  Partition& S = c->src;
+  h2d_narrow(S.start, start, nc, st, "cluster start");
+  h2d_narrow(S.stop, stop, nc, st, "cluster stop");
+  h2d_narrow(S.child_start, child_start, nc, st, "child_start");
+  h2d_narrow(S.child_count, child_count, nc, st, "child_count");
+  h2d(S.lo, lo, 3 * nc, st);
+  h2d(S.hi, hi, 3 * nc, st);
+  S.n_nodes = nc;
+  c->mac.resize(nc);
+  c->ecl.resize(nc);
+  k_mac_nodes<<<grid_for(nc, 128), 128, 0, st>>>(nc, S.lo.p, S.hi.p, S.start.p, S.stop.p,
+                                                 S.child_start.p, S.child_count.p, c->mac.p);
+  BLTC_LAUNCH_CHECK();
+  k_eval_clusters<<<grid_for(nc, 128), 128, 0, st>>>(nc, S.lo.p, S.hi.p, S.start.p, S.stop.p, 0,
+                                                     c->ecl.p);
+  BLTC_LAUNCH_CHECK();
+}
+
+void upload_batches(bltc_ctx* c, int64_t nb, const int64_t* bstart, const int64_t* bstop,
+                    const double* bcenter, const double* bradius) {
+  h2d_narrow(c->bstart, bstart, nb, c->st, "batch start");
+  h2d_narrow(c->bstop, bstop, nb, c->st, "batch stop");
+  c->bstart.n = c->bstop.n = nb;
+  h2d(c->bcenter, bcenter, 3 * nb, c->st);
+  h2d(c->bradius, bradius, nb, c->st);
+}
+
 }  // namespace
 
 extern "C" {
+
 
 const char* bltc_last_error(void) { return g_err.c_str(); }
 const char* bltc_version(void) { return "libbltc 0.1 (sm_100a)"; }
@@ -880,7 +950,7 @@ int bltc_export_batches(bltc_ctx* c, int64_t* start, int64_t* stop, double* cent
 int bltc_export_lists(bltc_ctx* c, int64_t* a_ptr, int64_t* a_idx, int64_t* d_ptr,
                       int64_t* d_idx) {
   return guarded([&] {
-    require_run(c);
+    if (!(c && c->lists_staged)) require_run(c);
     BLTC_CUDA(cudaSetDevice(c->device));
     const Lists& L = c->lists;
     const int64_t nseg = L.nb * L.n_groups;
@@ -1231,6 +1301,270 @@ int bltc_rank_evaluate(bltc_ctx* c, const bltc_params* p, int32_t ranks, int32_t
       stats->batch_depth = c->tgt->depth;
     }
     c->have_run = true;
+  });
+}
+
+// ---- Stage calls with host-provided upstream structures -------------------
+
+int bltc_stage_lists(bltc_ctx* c, const bltc_params* p, int64_t n_batches,
+                     const int64_t* batch_start, const int64_t* batch_stop,
+                     const double* batch_center, const double* batch_radius,
+                     int64_t n_clusters, const int64_t* start, const int64_t* stop,
+                     const double* lo, const double* hi, const int64_t* child_start,
+                     const int64_t* child_count, int64_t* n_approx, int64_t* n_direct) {
+  return guarded([&] {
+    if (!c) {
+      set_error("ctx is NULL");
+      throw UserError{BLTC_ERR_VALUE};
+    }
+    check_params(p);
+    BLTC_CUDA(cudaSetDevice(c->device));
+    if (n_batches < 1 || n_clusters < 1) {
+      set_error("need at least one batch and one cluster");
+      throw UserError{BLTC_ERR_VALUE};
+    }
+    for (const void* q : {(const void*)batch_start, (const void*)batch_stop,
+                          (const void*)batch_center, (const void*)batch_radius,
+                          (const void*)start, (const void*)stop, (const void*)lo,
+                          (const void*)hi, (const void*)child_start,
+                          (const void*)child_count})
+      require_ptr(q, "stage input");
+    c->have_run = false;
+    c->params = *p;
+    upload_batches(c, n_batches, batch_start, batch_stop, batch_center, batch_radius);
+    upload_tree(c, n_clusters, start, stop, lo, hi, child_start, child_count);
+    const MacNode* trees[1] = {c->mac.p};
+    const int32_t offs[1] = {0};
+    build_lists(c, p, 1, trees, offs);
+    BLTC_CUDA(cudaStreamSynchronize(c->st));
+    if (n_approx) *n_approx = c->lists.n_approx;
+    if (n_direct) *n_direct = c->lists.n_direct;
+    c->lists_staged = true;
+  });
+}
+
+int bltc_stage_moments(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64_t n_s,
+                       const double* sx, const double* sy, const double* sz, const double* q,
+                       int64_t n_clusters, const int64_t* start, const int64_t* stop,
+                       const double* lo, const double* hi, int64_t n_list,
+                       const int64_t* cluster_ids, double* rows_out) {
+  return guarded([&] {
+    if (!c) {
+      set_error("ctx is NULL");
+      throw UserError{BLTC_ERR_VALUE};
+    }
+    check_params(p);
+    BLTC_CUDA(cudaSetDevice(c->device));
+    if (n_s < 1 || n_clusters < 1) {
+      set_error("need at least one source and one cluster");
+      throw UserError{BLTC_ERR_VALUE};
+    }
+    for (const void* ptr : {(const void*)sx, (const void*)sy, (const void*)sz, (const void*)q,
+                            (const void*)start, (const void*)stop, (const void*)lo,
+                            (const void*)hi})
+      require_ptr(ptr, "stage input");
+    if (n_list > 0) {
+      require_ptr(cluster_ids, "cluster_ids");
+      require_ptr(rows_out, "rows_out");
+    }
+    c->have_run = false;
+    c->params = *p;
+    cudaStream_t st = c->st;
+    upload_nodes(c, p, cheb_s);
+    Partition& S = c->src;
+    h2d(S.x, sx, n_s, st);
+    h2d(S.y, sy, n_s, st);
+    h2d(S.z, sz, n_s, st);
+    h2d(S.q, q, n_s, st);
+    S.n = n_s;
+    h2d_narrow(S.start, start, n_clusters, st, "cluster start");
+    h2d_narrow(S.stop, stop, n_clusters, st, "cluster stop");
+    h2d(S.lo, lo, 3 * n_clusters, st);
+    h2d(S.hi, hi, 3 * n_clusters, st);
+    for (int64_t i = 0; i < n_list; ++i)
+      if (cluster_ids[i] < 0 || cluster_ids[i] >= n_clusters) {
+        set_error("cluster id out of range");
+        throw UserError{BLTC_ERR_VALUE};
+      }
+    h2d_narrow(c->mlist, cluster_ids, n_list, st, "cluster id");
+    if (n_list == 0) return;
+    const int m = p->degree + 1;
+    const int64_t m3 = (int64_t)m * m * m;
+    const int mstride = moment_stride(p->degree);
+    c->rows.resize(n_list * mstride + 2);
+    if (p->mode == BLTC_MODE_FAST) {
+      launch_moments_split(S.x.p, S.y.p, S.z.p, S.q.p, c->mlist.p, n_list, S.start.p, S.stop.p,
+                           S.lo.p, S.hi.p, c->s_nodes.p, c->w_nodes.p, p->degree, mstride,
+                           c->rows.p, c->item_cnt, c->item_off, c->items, c->partial,
+                           c->bs.scan_tmp, c->hs, st);
+    } else {
+      int threads = ((m * m + 31) / 32) * 32;
+      if (threads < 96) threads = 96;
+      k_moments<<<(unsigned)n_list, threads, 0, st>>>(S.x.p, S.y.p, S.z.p, S.q.p, c->mlist.p,
+                                                      S.start.p, S.stop.p, S.lo.p, S.hi.p,
+                                                      c->s_nodes.p, c->w_nodes.p, p->degree,
+                                                      mstride, c->rows.p);
+      BLTC_LAUNCH_CHECK();
+    }
+    BLTC_CUDA(cudaMemcpy2DAsync(rows_out, m3 * sizeof(double), c->rows.p,
+                                mstride * sizeof(double), m3 * sizeof(double), n_list,
+                                cudaMemcpyDeviceToHost, st));
+    BLTC_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int bltc_stage_potentials(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64_t n_t,
+                          const double* tx, const double* ty, const double* tz,
+                          int64_t n_batches, const int64_t* batch_start,
+                          const int64_t* batch_stop, const double* batch_center,
+                          const double* batch_radius, int64_t n_s, const double* sx,
+                          const double* sy, const double* sz, const double* q,
+                          int64_t n_clusters, const int64_t* start, const int64_t* stop,
+                          const double* lo, const double* hi, const int64_t* a_ptr,
+                          const int64_t* a_idx, const int64_t* d_ptr, const int64_t* d_idx,
+                          const int64_t* moment_row, int64_t n_rows, const double* rows,
+                          const int64_t* perm, double* phi_out, bltc_stats* stats) {
+  return guarded([&] {
+    if (!c) {
+      set_error("ctx is NULL");
+      throw UserError{BLTC_ERR_VALUE};
+    }
+    check_params(p);
+    BLTC_CUDA(cudaSetDevice(c->device));
+    if (n_t < 1 || n_s < 1 || n_batches < 1 || n_clusters < 1) {
+      set_error("need targets, sources, batches and clusters");
+      throw UserError{BLTC_ERR_VALUE};
+    }
+    for (const void* ptr : {(const void*)tx, (const void*)ty, (const void*)tz,
+                            (const void*)batch_start, (const void*)batch_stop,
+                            (const void*)batch_center, (const void*)batch_radius,
+                            (const void*)sx, (const void*)sy, (const void*)sz, (const void*)q,
+                            (const void*)start, (const void*)stop, (const void*)lo,
+                            (const void*)hi, (const void*)a_ptr, (const void*)d_ptr,
+                            (const void*)moment_row, (const void*)phi_out})
+      require_ptr(ptr, "stage input");
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    c->have_run = false;
+    c->params = *p;
+    cudaStream_t st = c->st;
+    const long long launches0 = g_launch_count;
+    Timer tm(c->timing, st);
+    upload_nodes(c, p, cheb_s);
+    tm.mark();
+    const int m = p->degree + 1;
+    const int64_t m3 = (int64_t)m * m * m;
+    const int mstride = moment_stride(p->degree);
+    // targets (batch order) and batches
+    Partition& T = c->tgt_own;
+    h2d(T.x, tx, n_t, st);
+    h2d(T.y, ty, n_t, st);
+    h2d(T.z, tz, n_t, st);
+    T.n = n_t;
+    c->tgt = &T;
+    upload_batches(c, n_batches, batch_start, batch_stop, batch_center, batch_radius);
+    // sources (cluster order) and clusters
+    Partition& S = c->src;
+    h2d(S.x, sx, n_s, st);
+    h2d(S.y, sy, n_s, st);
+    h2d(S.z, sz, n_s, st);
+    h2d(S.q, q, n_s, st);
+    S.n = n_s;
+    S.n_nodes = n_clusters;
+    std::vector<EvalCluster> ecl(n_clusters);
+    for (int64_t i = 0; i < n_clusters; ++i) {
+      EvalCluster& e = ecl[i];
+      for (int d = 0; d < 3; ++d) {
+        e.lo[d] = lo[3 * i + d];
+        e.hi[d] = hi[3 * i + d];
+      }
+      if (start[i] < 0 || stop[i] > n_s || start[i] > stop[i]) {
+        set_error("cluster particle range out of bounds");
+        throw UserError{BLTC_ERR_VALUE};
+      }
+      e.start = (int32_t)start[i];
+      e.stop = (int32_t)stop[i];
+      if (moment_row[i] >= n_rows) {
+        set_error("moment row out of range");
+        throw UserError{BLTC_ERR_VALUE};
+      }
+      e.mrow = (int32_t)moment_row[i];
+      e.pad = 0;
+    }
+    c->ecl.resize(n_clusters);
+    BLTC_CUDA(cudaMemcpyAsync(c->ecl.p, ecl.data(), n_clusters * sizeof(EvalCluster),
+                              cudaMemcpyHostToDevice, st));
+    // lists (single source group) and pair counts (engine.py:133-143)
+    Lists& L = c->lists;
+    const int64_t na = a_ptr[n_batches], nd = d_ptr[n_batches];
+    if ((na > 0 && !a_idx) || (nd > 0 && !d_idx)) {
+      set_error("list entries are NULL");
+      throw UserError{BLTC_ERR_VALUE};
+    }
+    unsigned long long approx_pairs = 0, direct_pairs = 0;
+    for (int64_t b = 0; b < n_batches; ++b) {
+      const int64_t nt_b = batch_stop[b] - batch_start[b];
+      for (int64_t e = a_ptr[b]; e < a_ptr[b + 1]; ++e) {
+        if (a_idx[e] < 0 || a_idx[e] >= n_clusters || moment_row[a_idx[e]] < 0) {
+          set_error("approximation entry without a moment row");
+          throw UserError{BLTC_ERR_VALUE};
+        }
+        approx_pairs += (unsigned long long)(nt_b * m3);
+      }
+      for (int64_t e = d_ptr[b]; e < d_ptr[b + 1]; ++e) {
+        if (d_idx[e] < 0 || d_idx[e] >= n_clusters) {
+          set_error("direct entry out of range");
+          throw UserError{BLTC_ERR_VALUE};
+        }
+        direct_pairs += (unsigned long long)(nt_b * (stop[d_idx[e]] - start[d_idx[e]]));
+      }
+    }
+    h2d_narrow(L.a_ptr, a_ptr, n_batches + 1, st, "a_ptr");
+    h2d_narrow(L.d_ptr, d_ptr, n_batches + 1, st, "d_ptr");
+    h2d_narrow(L.a_idx, a_idx, na, st, "a_idx");
+    h2d_narrow(L.d_idx, d_idx, nd, st, "d_idx");
+    L.nb = n_batches;
+    L.n_groups = 1;
+    L.n_approx = na;
+    L.n_direct = nd;
+    // moments, rows padded to the 16-byte stride
+    c->rows.resize(n_rows * mstride + 2);
+    if (n_rows > 0) {
+      require_ptr(rows, "rows");
+      BLTC_CUDA(cudaMemcpy2DAsync(c->rows.p, mstride * sizeof(double), rows,
+                                  m3 * sizeof(double), m3 * sizeof(double), n_rows,
+                                  cudaMemcpyHostToDevice, st));
+    }
+    if (p->mode == BLTC_MODE_FAST) {
+      c->src4.resize(n_s);
+      k_pack4<<<grid_for(n_s, 256), 256, 0, st>>>(n_s, S.x.p, S.y.p, S.z.p, S.q.p, c->src4.p);
+      BLTC_LAUNCH_CHECK();
+    }
+    tm.mark();
+    evaluate(c, p, 1, c->ecl.p, S.x.p, S.y.p, S.z.p, S.q.p, c->src4.p, c->rows.p, stats);
+    c->phi_dev.resize(n_t);
+    if (perm) {   // (out + carry)[perm] of compute_potentials (engine.py:335)
+      h2d_narrow(T.perm, perm, n_t, st, "perm");
+      k_unpermute<<<grid_for(n_t, 256), 256, 0, st>>>(n_t, c->out_sorted.p, T.perm.p,
+                                                      c->phi_dev.p);
+      BLTC_LAUNCH_CHECK();
+      BLTC_CUDA(cudaMemcpyAsync(phi_out, c->phi_dev.p, n_t * sizeof(double),
+                                cudaMemcpyDeviceToHost, st));
+    } else {
+      BLTC_CUDA(cudaMemcpyAsync(phi_out, c->out_sorted.p, n_t * sizeof(double),
+                                cudaMemcpyDeviceToHost, st));
+    }
+    tm.mark();
+    BLTC_CUDA(cudaStreamSynchronize(st));
+    if (stats) {
+      stats->n_clusters = n_clusters;
+      stats->n_batches = n_batches;
+      stats->direct_pairs = (int64_t)direct_pairs;
+      stats->approx_pairs = (int64_t)approx_pairs;
+      stats->compute_s = tm.secs(1, 2);
+      stats->total_s = tm.secs(0, 2);
+      stats->n_moments = n_rows;
+      stats->kernel_launches = g_launch_count - launches0;
+    }
   });
 }
 
