@@ -152,6 +152,49 @@ class Published:
                 int(self.moments.shape[0]))
 
 
+# ---------------------------------------------------------------------------
+# Collectives.  NCCL moves CUDA tensors directly over NVLink; a gloo group
+# (CPU tests, or several ranks sharing one GPU) gets host copies.
+
+
+def _via_host(t, group) -> bool:
+    import torch.distributed as dist
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
+def _all_gather(out_list, t, group=None):
+    import torch
+    import torch.distributed as dist
+    if _via_host(t, group):
+        outs = [torch.empty(o.shape, dtype=o.dtype) for o in out_list]
+        dist.all_gather(outs, t.cpu(), group=group)
+        for o, h in zip(out_list, outs):
+            o.copy_(h)
+    else:
+        dist.all_gather(out_list, t, group=group)
+
+
+def _all_to_all_single(out, inp, out_split=None, in_split=None, group=None):
+    import torch
+    import torch.distributed as dist
+    if _via_host(inp, group):
+        h = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_to_all_single(h, inp.cpu(), out_split, in_split, group=group)
+        out.copy_(h)
+    else:
+        dist.all_to_all_single(out, inp, out_split, in_split, group=group)
+
+
+def _all_reduce(t, group=None):
+    import torch.distributed as dist
+    if _via_host(t, group):
+        h = t.cpu()
+        dist.all_reduce(h, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, group=group)
+
+
 def all_gather_published(pub: Published, ranks: int, group=None) -> list[Published]:
     """Replicate every rank's published data on every rank: one size
     all-gather, then one padded all-gather per buffer (NCCL over NVLink for
@@ -162,7 +205,7 @@ def all_gather_published(pub: Published, ranks: int, group=None) -> list[Publish
     dev = pub.records.device
     sizes = torch.tensor(pub.sizes, dtype=torch.int64, device=dev)
     all_sizes = [torch.empty_like(sizes) for _ in range(ranks)]
-    dist.all_gather(all_sizes, sizes, group=group)
+    _all_gather(all_sizes, sizes, group=group)
     all_sizes = [tuple(int(v) for v in s.tolist()) for s in all_sizes]
     ncols = pub.moments.shape[1]
     out = []
@@ -175,7 +218,7 @@ def all_gather_published(pub: Published, ranks: int, group=None) -> list[Publish
         mine = getattr(pub, key).reshape(-1)
         buf[:mine.numel()] = mine
         gathered = [torch.empty_like(buf) for _ in range(ranks)]
-        dist.all_gather(gathered, buf, group=group)
+        _all_gather(gathered, buf, group=group)
         flat[key] = (gathered, counts)
     for r in range(ranks):
         nc, n, nrow = all_sizes[r]
@@ -195,13 +238,13 @@ def all_gather_records(pub: Published, ranks: int, group=None) -> list:
     dev = pub.records.device
     n = torch.tensor([pub.records.shape[0]], dtype=torch.int64, device=dev)
     sizes = [torch.empty_like(n) for _ in range(ranks)]
-    dist.all_gather(sizes, n, group=group)
+    _all_gather(sizes, n, group=group)
     sizes = [int(v.item()) for v in sizes]
     cap = max(1, max(sizes)) * RECORD_DOUBLES
     buf = torch.zeros(cap, dtype=torch.float64, device=dev)
     buf[:pub.records.numel()] = pub.records.reshape(-1)
     gathered = [torch.empty_like(buf) for _ in range(ranks)]
-    dist.all_gather(gathered, buf, group=group)
+    _all_gather(gathered, buf, group=group)
     return [gathered[r][:sizes[r] * RECORD_DOUBLES].view(sizes[r], RECORD_DOUBLES)
             for r in range(ranks)]
 
@@ -359,13 +402,13 @@ def let_exchange(pub: Published, needs_fn, ranks: int, me: int, group=None):
     cnt = torch.tensor([[plan.na[o], plan.nd[o]] if o != me else [0, 0] for o in range(ranks)],
                        dtype=torch.int64, device=dev)
     rcnt = torch.empty_like(cnt)
-    dist.all_to_all_single(rcnt, cnt, group=group)
+    _all_to_all_single(rcnt, cnt, group=group)
     rcnt_h = rcnt.cpu().tolist()
     send_ids = torch.cat([torch.cat([plan.a[o], plan.d[o]]) for o in range(ranks)])
     in_split = [plan.na[o] + plan.nd[o] if o != me else 0 for o in range(ranks)]
     out_split = [sum(c) for c in rcnt_h]
     recv_ids = torch.empty(sum(out_split), dtype=torch.int64, device=dev)
-    dist.all_to_all_single(recv_ids, send_ids, out_split, in_split, group=group)
+    _all_to_all_single(recv_ids, send_ids, out_split, in_split, group=group)
     # serve every requester
     reqs, pos = [], 0
     for r in range(ranks):
@@ -380,7 +423,7 @@ def let_exchange(pub: Published, needs_fn, ranks: int, me: int, group=None):
     fetch_split = [plan.na[o] * ncols + 4 * plan.npart[o] if o != me else 0
                    for o in range(ranks)]
     recv = torch.empty(sum(fetch_split), dtype=torch.float64, device=dev)
-    dist.all_to_all_single(recv, send, fetch_split, serve_split, group=group)
+    _all_to_all_single(recv, send, fetch_split, serve_split, group=group)
     forest, fetch, pos = [], {}, 0
     for o in range(ranks):
         if o == me:
@@ -450,7 +493,10 @@ class DeviceRankEngine:
         from .engine import Context, make_params
         self.torch = torch
         self.device = torch.cuda.current_device() if device is None else int(device)
-        self.ctx = context or Context(self.device)
+        # libbltc runs on torch's current stream, so the tensors this engine
+        # hands it (inputs, exchanged buffers) are stream-ordered with it
+        self.ctx = context or Context(self.device,
+                                      torch.cuda.current_stream(self.device).cuda_stream)
         self.params = make_params(config, mode, all_moments=False)
         self.n = 0
         self.stats = None
@@ -462,6 +508,7 @@ class DeviceRankEngine:
                                         if not isinstance(v, torch.Tensor) else v,
                                         device=dev).contiguous() for v in (x, y, z, q)]
         self.n = int(self._inputs[0].shape[0])
+        self._sync()
         self.ctx.rank_build(self.params, self.n, *[t.data_ptr() for t in self._inputs],
                             device_ptrs=True)
 
@@ -473,9 +520,15 @@ class DeviceRankEngine:
         par = torch.empty((4, sz["n_particles"]), dtype=torch.float64, device=dev)
         mom = torch.empty((max(1, sz["n_moment_rows"]), moment_stride(self.params.degree)),
                           dtype=torch.float64, device=dev)
+        self._sync()
         self.ctx.rank_publish(rec.data_ptr(), par.data_ptr(), mom.data_ptr())
         torch.cuda.synchronize(dev)
         return Published(rec, par, mom[:sz["n_moment_rows"]])
+
+    def _sync(self):
+        """Order torch's work before libbltc's when the context has its own
+        stream (a caller-supplied context)."""
+        self.torch.cuda.current_stream(self.device).synchronize()
 
     def needs(self, ranks: int, my_rank: int, records: list) -> list:
         """LET step one on the device: per owner, int32 need flags per cluster."""
@@ -484,6 +537,7 @@ class DeviceRankEngine:
         sizes = [int(r.shape[0]) for r in records]
         recs = [r.to(dev).contiguous() for r in records]
         flags = torch.empty(max(1, sum(sizes)), dtype=torch.int32, device=dev)
+        self._sync()
         self.ctx.rank_needs(self.params, ranks, my_rank, sizes, [r.data_ptr() for r in recs],
                             flags.data_ptr())
         out, pos = [], 0
@@ -500,6 +554,7 @@ class DeviceRankEngine:
         # zero-row moment tensors still need a valid pointer
         mom_ptrs = [p.moments.data_ptr() if p.moments.numel() else p.records.data_ptr()
                     for p in forest]
+        self._sync()
         self.stats = self.ctx.rank_evaluate(
             self.params, ranks, my_rank, [s[0] for s in sizes], [s[1] for s in sizes],
             [s[2] for s in sizes], [p.records.data_ptr() for p in forest],
@@ -631,11 +686,11 @@ def run_distributed(system, config, ranks: int, threads: int = 1, mode: str | No
         mine_phi = rank_phi[me].reshape(-1)
         buf[:mine_phi.numel()] = mine_phi
         gathered = [torch.empty_like(buf) for _ in range(ranks)]
-        dist.all_gather(gathered, buf, group=group)
+        _all_gather(gathered, buf, group=group)
         for o in range(ranks):
             phi[part.rank_indices(o)] = gathered[o][:counts[o]].cpu().numpy()
         tot = torch.tensor(local, dtype=torch.int64, device=dev)
-        dist.all_reduce(tot, group=group)
+        _all_reduce(tot, group=group)
         local = tot.cpu().numpy()
     else:
         for o in range(ranks):
