@@ -128,8 +128,17 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 
-def make_system(cfg: dict, seed: int = 1):
+def make_system(cfg: dict, seed: int = 1, device: int | None = None):
+    """The workload's particles.  Uniform cubes are generated on the GPU when
+    ``device`` is given (bltc_philox_uniform: numpy's Philox stream bit for
+    bit, tests/test_gpu_generate.py), then copied to the host; Plummer and the
+    CPU reference arm use numpy."""
     from paper_2003_01836_b200 import cli
+    if cfg["gen"] == "uniform" and device is not None:
+        from paper_2003_01836_b200.particles import ParticleSystem, Points
+        x, y, z, q = (t.cpu().numpy() for t in cli.generate_particles_device(cfg["n"], seed,
+                                                                            device))
+        return ParticleSystem.from_single_set(Points(x, y, z), q)
     gen = cli.generate_particles if cfg["gen"] == "uniform" else cli.generate_plummer
     return gen(cfg["n"], seed)
 
@@ -322,7 +331,7 @@ def run_ours(args, cfg):
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     econf = eval_config(cfg, args.batch_size, args.leaf_size)
-    system = make_system(cfg)
+    system = make_system(cfg, device=local)
     n = cfg["n"]
     stream = torch.cuda.current_stream()
     ctx = bltc.Context(local, stream.cuda_stream)

@@ -244,6 +244,15 @@ BLTC_API int bltc_direct_sum(bltc_ctx* ctx, int32_t kernel_code, double kappa, i
                              const double* sy, const double* sz, const double* q,
                              double* out);
 
+/* ---- Input generation on the device (cli.py:54-62) ----
+ * numpy's Generator(Philox).uniform(low, high, (n, dims)) stream, bit for bit,
+ * from the bit generator's key[2] and counter[4] (numpy state, read on the
+ * host): draw j goes to out[j % dims][j / dims].  out: dims device pointers
+ * of n doubles.  Runs on the default stream and synchronises. */
+BLTC_API int bltc_philox_uniform(int device, const uint64_t* key, const uint64_t* counter,
+                                 int64_t n, int32_t dims, double low, double high,
+                                 double* const* out);
+
 /* ---- Diagnostics --------------------------------------------------------
  * Sustained FP64 FMA throughput of the device (DFMA/s), measured for about
  * `seconds`: the denominator of the FP64 roofline fraction bench.py reports. */

@@ -118,3 +118,33 @@ def test_full_oracle_refusal_before_device():
     with pytest.raises(cli.OracleTooLarge):
         cli.direct_sum_oracle(ParticleSystem.from_single_set(pts, np.ones(n)),
                               __import__("paper_2003_01836_b200").coulomb())
+
+
+def test_philox_model_matches_numpy():
+    """The Philox4x64-10 model the device generator implements (counter
+    incremented before each 4-word block, u >> 11 scaled by 2^-53)
+    reproduces numpy's uniform stream from the exported key / counter."""
+    from numpy.random import Generator, Philox, SeedSequence
+    M0, M1 = 0xD2E7470EE14C6C93, 0xCA5A826395121157
+    W0, W1 = 0x9E3779B97F4A7C15, 0xBB67AE8584CAA73B
+    MASK = (1 << 64) - 1
+
+    def block(c, k):
+        c, k = list(c), list(k)
+        for r in range(10):
+            if r:
+                k = [(k[0] + W0) & MASK, (k[1] + W1) & MASK]
+            p0, p1 = M0 * c[0], M1 * c[2]
+            c = [(p1 >> 64) ^ c[1] ^ k[0], p1 & MASK, (p0 >> 64) ^ c[3] ^ k[1], p0 & MASK]
+        return c
+
+    child = SeedSequence(12345).spawn(2)[0]
+    key, ctr = cli.philox_state(child)
+    c = [int(v) for v in ctr]
+    words = []
+    for _ in range(4):
+        c[0] = (c[0] + 1) & MASK
+        words += block(c, [int(v) for v in key])
+    mine = np.array([-1.0 + 2.0 * ((u >> 11) * (1.0 / 9007199254740992.0)) for u in words[:15]])
+    ref = Generator(Philox(child)).uniform(-1.0, 1.0, (5, 3)).ravel()
+    np.testing.assert_array_equal(mine, ref)
