@@ -61,7 +61,9 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
         obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + hdrs + [__file__]):
-            cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj]
+            # BLTC_NVCC_DEFS: extra -D flags for tuning builds (e.g. "-DBLTC_GMAX=6")
+            extra = os.environ.get("BLTC_NVCC_DEFS", "").split()
+            cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra, "-c", src, "-o", obj]
             if ptxas_v:
                 cmd += ["-Xptxas", "-v"]
             jobs.append(cmd)

@@ -34,7 +34,10 @@ namespace bltc {
 
 namespace {
 constexpr int kWarps = 8;     // warps per CTA
-constexpr int kGMax = 4;      // batches (segments) per work item
+#ifndef BLTC_GMAX
+#define BLTC_GMAX 4
+#endif
+constexpr int kGMax = BLTC_GMAX;   // batches (segments) per work item
 constexpr int kSlots = 64;    // target slots per item: 2 per lane
 constexpr int kNearCh = 32;   // near field default: sources per staged chunk and segment
 
