@@ -28,7 +28,9 @@
 #include "bltc_internal.cuh"
 #include "eval_common.cuh"
 
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 namespace bltc {
 
@@ -206,6 +208,9 @@ __global__ void k_direct_mask(int64_t nb, int G, const int32_t* d_ptr, const int
       g2 = fma(g, g, g2);
     }
     mask[e] = (sqrt(g2) - br) <= 1e-12 * (1.0 + scale) ? 1 : 0;
+#ifdef BLTC_DEBUG_NOMASK
+    mask[e] = 0;   // timing experiment only: wrong results for singular pairs
+#endif
   }
 }
 
@@ -731,6 +736,15 @@ void build_packed_items(const EvalArgs& a, DBuf<int32_t>& pc, DBuf<int32_t>& pof
                                                             a.clusters, a.bcenter, a.bradius,
                                                             dmask.p);
     BLTC_LAUNCH_CHECK();
+    if (std::getenv("BLTC_TRACE_MASK")) {   // diagnostic: share of masked entries
+      std::vector<uint8_t> hm(n_direct);
+      BLTC_CUDA(cudaMemcpyAsync(hm.data(), dmask.p, n_direct, cudaMemcpyDeviceToHost, st));
+      BLTC_CUDA(cudaStreamSynchronize(st));
+      int64_t on = 0;
+      for (auto v : hm) on += v;
+      std::fprintf(stderr, "[bltc] direct entries %lld, singular-mask flagged %lld\n",
+                   (long long)n_direct, (long long)on);
+    }
   }
   out->items = items.p;
   out->poff = poff.p;

@@ -200,7 +200,6 @@ def all_gather_published(pub: Published, ranks: int, group=None) -> list[Publish
     all-gather, then one padded all-gather per buffer (NCCL over NVLink for
     CUDA tensors, gloo for CPU tensors)."""
     import torch
-    import torch.distributed as dist
 
     dev = pub.records.device
     sizes = torch.tensor(pub.sizes, dtype=torch.int64, device=dev)
@@ -233,7 +232,6 @@ def all_gather_records(pub: Published, ranks: int, group=None) -> list:
     """LET step one's collective: every rank's tree records on every rank
     (one size all-gather, one padded all-gather)."""
     import torch
-    import torch.distributed as dist
 
     dev = pub.records.device
     n = torch.tensor([pub.records.shape[0]], dtype=torch.int64, device=dev)
@@ -392,7 +390,6 @@ def let_exchange(pub: Published, needs_fn, ranks: int, me: int, group=None):
     (forest in owner order -- own data for ``me``, fetched data otherwise --
     and {(me, owner): FetchStats})."""
     import torch
-    import torch.distributed as dist
 
     dev = pub.records.device
     ncols = int(pub.moments.shape[1])
