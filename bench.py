@@ -208,10 +208,11 @@ class CpuReference:
 
     def step(self) -> dict:
         t0 = time.perf_counter()
-        self.orc.evaluate(self.batches, [self.orc.SourceGroup(self.tree, self.rows, self.mrow,
-                                                               self.lists)],
-                          self.econf.degree, self.econf.kernel.code, self.econf.kernel.kappa,
-                          self.threads, sel=self.sel)
+        self.last = self.orc.evaluate(self.batches,
+                                      [self.orc.SourceGroup(self.tree, self.rows, self.mrow,
+                                                            self.lists)],
+                                      self.econf.degree, self.econf.kernel.code,
+                                      self.econf.kernel.kappa, self.threads, sel=self.sel)
         t = time.perf_counter() - t0
         est = self.setup_s + self.moments_s + t / self.frac
         return {"value": self.system.n_targets / est, "unit": "particles/s",
@@ -225,6 +226,26 @@ class CpuReference:
                 "est_step_s": est}
 
 
+    def sampled_parity(self, phi_parity, phi_fast) -> dict:
+        """Full-size parity on the sampled batches: the CPU restatement's
+        potentials of every target in the evaluated sample against the GPU's
+        PARITY (bitwise expected) and FAST results."""
+        b = self.batches
+        pos = np.concatenate([np.arange(b.start[i], b.stop[i]) for i in self.sel])
+        out, carry = self.last
+        ref = (out + carry)[pos]
+        orig = b.tree.order[pos]
+        dp = np.abs(phi_parity[orig] - ref)
+        df = np.abs(phi_fast[orig] - ref)
+        nz = ref != 0
+        return {"targets": int(pos.shape[0]), "batches": int(len(self.sel)),
+                "parity_bitwise_equal": bool(np.array_equal(phi_parity[orig], ref)),
+                "parity_max_abs_diff": float(dp.max()),
+                "fast_condition_aware": float(df.max() / np.abs(ref).max()),
+                "fast_strict_max_rel": float((df[nz] / np.abs(ref[nz])).max()),
+                "fast_frac_targets_above_1e-10": float((df[nz] / np.abs(ref[nz]) > 1e-10).mean())}
+
+
 def cpu_baseline(system, cfg, econf, budget_pairs: float = 1.5e10):
     return CpuReference(system, econf, budget_pairs).step()
 
@@ -232,7 +253,7 @@ def cpu_baseline(system, cfg, econf, budget_pairs: float = 1.5e10):
 # ---------------------------------------------------------------------------
 
 
-def accuracy_block(ctx, system, econf, mode, phi, args) -> dict:
+def accuracy_block(ctx, system, econf, mode, phi, args, cpu_ref=None) -> dict:
     """Accuracy of the timed result at the full workload size.
 
     * relative L2 error against a direct sum on the reference harness's
@@ -261,7 +282,11 @@ def accuracy_block(ctx, system, econf, mode, phi, args) -> dict:
     d = np.abs(phi - phi_p)
     nz = phi_p != 0
     strict = float((d[nz] / np.abs(phi_p[nz])).max()) if nz.any() else 0.0
+    sampled = None
+    if cpu_ref is not None and getattr(cpu_ref, "last", None) is not None:
+        sampled = cpu_ref.sampled_parity(phi_p, phi)
     return {"sample": int(sample.shape[0]), "error": err, "error_parity_mode": err_p,
+            "full_size_parity_vs_cpu_reference": sampled,
             "error_ratio": err / err_p if err_p else None,
             "vs_parity_strict_max_rel": strict,
             "vs_parity_condition_aware": float(d.max() / np.abs(phi_p).max()),
@@ -493,18 +518,20 @@ def run_ours(args, cfg):
         line["roofline"]["frac_nominal"] = far_tflops / nominal_tflops
     if e2e is not None:
         line["e2e"] = e2e
-    if dist is None and not args.no_accuracy:
-        try:
-            line["accuracy"] = accuracy_block(ctx, system, econf, mode, out, args)
-        except Exception as exc:   # reported, never required for the timing line
-            line["accuracy"] = {"error": repr(exc)}
+    cpu_ref = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            cb = cpu_baseline(system, cfg, econf, budget_pairs=args.ref_budget)
+            cpu_ref = CpuReference(system, econf, budget_pairs=args.ref_budget)
+            cb = cpu_ref.step()
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind",
                                                       "sample")}
         except Exception as exc:   # the baseline is reported, never required
             line["cpu_baseline"] = {"value": None, "error": repr(exc)}
+    if dist is None and not args.no_accuracy:
+        try:
+            line["accuracy"] = accuracy_block(ctx, system, econf, mode, out, args, cpu_ref)
+        except Exception as exc:   # reported, never required for the timing line
+            line["accuracy"] = {"error": repr(exc)}
     print(json.dumps(line), flush=True)
     ctx.close()
     if dist is not None:
