@@ -266,3 +266,26 @@ def test_fast_moments_close(bltc, ctx, case):
     ref = g["moments"][elig]
     scale = np.abs(ref).max(axis=1, keepdims=True) + 1e-300
     assert (np.abs(rows - ref) / scale).max() <= 1e-13
+
+
+@pytest.mark.parametrize("batch,leaf,deg", [(1, 8, 4), (2, 16, 5), (3, 40, 7), (7, 7, 8),
+                                            (33, 64, 10), (65, 100, 8)])
+def test_packed_items_ragged_batches(bltc, batch, leaf, deg):
+    """Packed FAST items over windows spanning many tiny batches (odd sizes,
+    one-target batches, windows split by the segment limit): FAST agrees with
+    PARITY (the reference's arithmetic), also forced onto the packed path."""
+    import os
+    from paper_2003_01836_b200 import cli
+    s = cli.generate_plummer(6000, 17)
+    cfg = bltc.EvalConfig(theta=0.7, degree=deg, leaf_size=leaf, batch_size=batch)
+    ref, _ = bltc.treecode_potentials(s, cfg, mode="parity")
+    for force in ("", "1"):
+        if force:
+            os.environ["BLTC_PACK"] = force
+        try:
+            phi, st = bltc.treecode_potentials(s, cfg, mode="fast")
+        finally:
+            os.environ.pop("BLTC_PACK", None)
+        _phi_check(phi, ref, 0, exact=False)
+        if force and deg + 1 in (5, 6, 8, 9, 11):
+            assert st.packed == 1
