@@ -513,7 +513,28 @@ void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, 
   a.kappa = p->kappa;
   c->out_sorted.resize(T.n);
   a.out = c->out_sorted.p;
-  if (p->mode == BLTC_MODE_PARITY) {
+  const bool parity_packed = p->mode == BLTC_MODE_PARITY && G == 1 &&
+                             packed_supported(p->kernel_code, p->degree) &&
+                             !(std::getenv("BLTC_PARITY_PACKED") &&
+                               std::atoi(std::getenv("BLTC_PARITY_PACKED")) == 0);
+  if (parity_packed) {
+    // bitwise-reference arithmetic on the packed work items: far partials,
+    // then the direct sums continuing them (eval_packed.cu, PAR)
+    c->far_out.resize(T.n);
+    a.far_out = c->far_out.p;
+    c->counters.resize(2);
+    PackedItems pi;
+    build_packed_items(a, c->pk_pc, c->pk_poff, c->pk_wcnt, c->pk_woff, c->pk_items,
+                       c->pk_dmask, c->lists.n_direct, c->bs.scan_tmp, c->hs, st, &pi);
+    float far_ms = 0, near_ms = 0;
+    launch_eval_packed(a, p->kernel_code, pi, c->counters.p, st, &far_ms, &near_ms, c->timing,
+                       true);
+    if (stats) {
+      stats->far_s = far_ms * 1e-3;
+      stats->near_s = near_ms * 1e-3;
+      stats->packed = 1;
+    }
+  } else if (p->mode == BLTC_MODE_PARITY) {
     launch_eval_parity(a, p->kernel_code, st);
   } else {
     c->far_out.resize(T.n);
@@ -632,7 +653,7 @@ void run_pipeline(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64
   tr("moments");
   tm.mark();  // 2
   // ---- compute: evaluation + un-permute
-  if (p->mode == BLTC_MODE_FAST) {
+  {   // packed (x, y, z, q) records: FAST and the packed PARITY kernels
     c->src4.resize(n_s);
     k_pack4<<<grid_for(n_s, 256), 256, 0, st>>>(n_s, c->src.x.p, c->src.y.p, c->src.z.p,
                                                 c->src.q.p, c->src4.p);
@@ -1266,7 +1287,7 @@ int bltc_rank_evaluate(bltc_ctx* c, const bltc_params* p, int32_t ranks, int32_t
     c->params = *p;
     build_lists(c, p, G, trees.data(), cl_off.data());
     tm.mark();
-    if (p->mode == BLTC_MODE_FAST) {
+    {   // packed (x, y, z, q) records: FAST and the packed PARITY kernels
       c->f_src4.resize(P);
       k_pack4<<<grid_for(P, 256), 256, 0, st>>>(P, c->f_x.p, c->f_y.p, c->f_z.p, c->f_q.p,
                                                 c->f_src4.p);
@@ -1534,7 +1555,7 @@ int bltc_stage_potentials(bltc_ctx* c, const bltc_params* p, const double* cheb_
                                   m3 * sizeof(double), m3 * sizeof(double), n_rows,
                                   cudaMemcpyHostToDevice, st));
     }
-    if (p->mode == BLTC_MODE_FAST) {
+    {   // packed (x, y, z, q) records: FAST and the packed PARITY kernels
       c->src4.resize(n_s);
       k_pack4<<<grid_for(n_s, 256), 256, 0, st>>>(n_s, S.x.p, S.y.p, S.z.p, S.q.p, c->src4.p);
       BLTC_LAUNCH_CHECK();

@@ -79,6 +79,15 @@ __device__ __forceinline__ double pair_acc(double acc, double q, double d2, doub
   return fma(__dmul_rn(q, ex), y, acc);
 }
 
+// PARITY: the reference tiles' term, IEEE sqrt / division, no contraction
+// (engine.py:183-191, 240-244).
+template <int KIND>
+__device__ __forceinline__ double parity_term(double q, double d2, double kappa) {
+  if (KIND == 0) return __ddiv_rn(q, __dsqrt_rn(d2));
+  const double r = __dsqrt_rn(d2);
+  return __ddiv_rn(__dmul_rn(exp(__dmul_rn(-kappa, r)), q), r);
+}
+
 __device__ __forceinline__ void neumaier(double& acc, double& comp, double t) {
   const double s = __dadd_rn(acc, t);
   const bool big = fabs(acc) >= fabs(t);
@@ -278,7 +287,10 @@ __device__ __forceinline__ void far_stage_slab(double* wsm, const FarHdr* H, int
   cp_async_commit();
 }
 
-template <int KIND, int M, int KU, int FORM>
+// PAR: bitwise the reference's _approx_tile (per cluster a plain sum in k1,
+// k2, k3 order, then out += acc per cluster in list order): d2 unfused,
+// IEEE sqrt / division.
+template <int KIND, int M, int KU, int FORM, bool PAR = false>
 __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it,
                                                 const int32_t* poff, double* wsm, int lane) {
   using SM = FarSmem<M>;
@@ -369,27 +381,29 @@ __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
           const double dy = __dsub_rn(ty[t], p2);
-          dxy2[t] = fma(dy, dy, dx2[t]);
+          dxy2[t] = PAR ? __dadd_rn(dx2[t], __dmul_rn(dy, dy)) : fma(dy, dy, dx2[t]);
         }
 #pragma unroll
         for (int k3 = 0; k3 < M; ++k3) {
           const double qv = qr[k3];
 #pragma unroll
-          for (int t = 0; t < 2; ++t)
-            part[t] = pair_acc<KIND, FORM>(part[t], qv, __dadd_rn(dxy2[t], dz2[t][k3]),
-                                           a.kappa);
+          for (int t = 0; t < 2; ++t) {
+            const double d2 = __dadd_rn(dxy2[t], dz2[t][k3]);
+            if (PAR) part[t] = __dadd_rn(part[t], parity_term<KIND>(qv, d2, a.kappa));
+            else part[t] = pair_acc<KIND, FORM>(part[t], qv, d2, a.kappa);
+          }
         }
       }
       __syncwarp();
     }
 #pragma unroll
-    for (int t = 0; t < 2; ++t) acc[t] = __dadd_rn(acc[t], act ? part[t] : 0.0);
+    for (int t = 0; t < 2; ++t) acc[t] = act ? __dadd_rn(acc[t], part[t]) : acc[t];
   }
   if (L.v0) a.far_out[L.i0] = acc[0];
   if (L.v1) a.far_out[L.i1] = acc[1];
 }
 
-template <int KIND, int M, int MINB, int KU, int FORM>
+template <int KIND, int M, int MINB, int KU, int FORM, bool PAR = false>
 __global__ void __launch_bounds__(kWarps * 32, MINB)
 k_far_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int32_t* poff,
              int* counter) {
@@ -397,7 +411,7 @@ k_far_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int3
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* wsm = smem + warp * FarSmem<M>::kWarp;
   for (int item = next_item(counter); item < n_items; item = next_item(counter))
-    far_packed_item<KIND, M, KU, FORM>(a, items[item], poff, wsm, lane);
+    far_packed_item<KIND, M, KU, FORM, PAR>(a, items[item], poff, wsm, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -432,6 +446,37 @@ __device__ __forceinline__ void near_chunk(double (&part)[2], const double4* src
         const double d2 = fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx)));
         part[t] = pair_acc<KIND, FORM>(part[t], s.w, d2, kappa);
       }
+    }
+  }
+}
+
+// PARITY: the reference's _direct_tile pair by pair -- d2 unfused, pairs with
+// d2 < 1e-28 skipped, Neumaier into (acc, comp) (engine.py:166-213).  The
+// zero-charge padding records add +0 exactly (acc and comp are never -0).
+template <int KIND, int CH, bool MASKED>
+__device__ __forceinline__ void near_chunk_parity(double (&acc)[2], double (&comp)[2],
+                                                  const double4* src, const double (&tx)[2],
+                                                  const double (&ty)[2],
+                                                  const double (&tz)[2], double kappa) {
+  const long long tb = __double_as_longlong(kSingularSq);
+#pragma unroll 2
+  for (int j = 0; j < CH; ++j) {
+    const double4 s = src[j];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const double dx = __dsub_rn(tx[t], s.x);
+      const double dy = __dsub_rn(ty[t], s.y);
+      const double dz = __dsub_rn(tz[t], s.z);
+      const double d2 =
+          __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+      const bool ok = !MASKED || __double_as_longlong(d2) >= tb;
+      const double term = parity_term<KIND>(s.w, ok ? d2 : 1.0, kappa);
+      const double sum = __dadd_rn(acc[t], term);
+      const bool big = fabs(acc[t]) >= fabs(term);
+      const double hi = big ? acc[t] : term, lo = big ? term : acc[t];
+      const double c2 = __dadd_rn(comp[t], __dadd_rn(__dsub_rn(hi, sum), lo));
+      acc[t] = ok ? sum : acc[t];
+      comp[t] = ok ? c2 : comp[t];
     }
   }
 }
@@ -540,7 +585,11 @@ __device__ __forceinline__ bool near_stage(const EvalArgs& a, const uint8_t* dma
   return __any_sync(0xffffffffu, need_mask);
 }
 
-template <int KIND, int CH, int FORM>
+// PAR: the direct sums continue the far-field value of each target with
+// per-pair Neumaier compensation, out = acc + carry at the end (engine.py:
+// 302-312, 335) -- valid for one source group (the distributed forest's
+// per-owner interleaving goes through k_eval_parity).
+template <int KIND, int CH, int FORM, bool PAR = false>
 __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 it,
                                                  const int32_t* poff, const uint8_t* dmask,
                                                  double4* wsm, int lane) {
@@ -549,6 +598,10 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
   const double ty[2] = {a.ty[L.i0], a.ty[L.i1]};
   const double tz[2] = {a.tz[L.i0], a.tz[L.i1]};
   double acc[2] = {0.0, 0.0}, comp[2] = {0.0, 0.0};
+  if (PAR) {
+    acc[0] = a.far_out[L.i0];
+    acc[1] = a.far_out[L.i1];
+  }
 
   Stream S[kGMax];
 #pragma unroll
@@ -580,13 +633,20 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
         cp_async_wait<0>();
       }
       __syncwarp();
-      double part[2] = {0.0, 0.0};
-      if (masked)
-        near_chunk<KIND, CH, true, FORM>(part, mine + buf * CH, tx, ty, tz, a.kappa);
-      else
-        near_chunk<KIND, CH, false, FORM>(part, mine + buf * CH, tx, ty, tz, a.kappa);
+      if constexpr (PAR) {
+        if (masked)
+          near_chunk_parity<KIND, CH, true>(acc, comp, mine + buf * CH, tx, ty, tz, a.kappa);
+        else
+          near_chunk_parity<KIND, CH, false>(acc, comp, mine + buf * CH, tx, ty, tz, a.kappa);
+      } else {
+        double part[2] = {0.0, 0.0};
+        if (masked)
+          near_chunk<KIND, CH, true, FORM>(part, mine + buf * CH, tx, ty, tz, a.kappa);
+        else
+          near_chunk<KIND, CH, false, FORM>(part, mine + buf * CH, tx, ty, tz, a.kappa);
 #pragma unroll
-      for (int t = 0; t < 2; ++t) neumaier(acc[t], comp[t], part[t]);
+        for (int t = 0; t < 2; ++t) neumaier(acc[t], comp[t], part[t]);
+      }
       __syncwarp();
       if (!more) break;
       masked = masked_next;
@@ -594,6 +654,11 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
   }
   // approximations first, then the compensated direct sums on top
   // (engine.py:302-312, 335)
+  if (PAR) {
+    if (L.v0) a.out[L.i0] = __dadd_rn(acc[0], comp[0]);
+    if (L.v1) a.out[L.i1] = __dadd_rn(acc[1], comp[1]);
+    return;
+  }
   if (L.v0) {
     double total = acc[0], cmp = comp[0];
     neumaier(total, cmp, a.far_out[L.i0]);
@@ -606,7 +671,7 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
   }
 }
 
-template <int KIND, int CH, int MINB, int FORM>
+template <int KIND, int CH, int MINB, int FORM, bool PAR = false>
 __global__ void __launch_bounds__(kWarps * 32, MINB)
 k_near_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int32_t* poff,
               const uint8_t* dmask, int* counter) {
@@ -615,7 +680,7 @@ k_near_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double4* wsm = smem + warp * NearSmem<CH>::kWarp;
   for (int item = next_item(counter); item < n_items; item = next_item(counter))
-    near_packed_item<KIND, CH, FORM>(a, items[item], poff, dmask, wsm, lane);
+    near_packed_item<KIND, CH, FORM, PAR>(a, items[item], poff, dmask, wsm, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -640,14 +705,27 @@ int persistent_grid(K kernel, int threads, size_t smem) {
   return sms * (per_sm > 0 ? per_sm : 1);
 }
 
-template <int KIND, int M, int KU = 1, int FORM = 0, int MINB = 2>
+template <int KIND, int M, int KU = 1, int FORM = 0, int MINB = 2, bool PAR = false>
 void far_packed_launch(const EvalArgs& a, const PackedItems& it, int* counter, cudaStream_t st) {
   const size_t smem = sizeof(double) * kWarps * FarSmem<M>::kWarp;
-  auto kern = k_far_packed<KIND, M, MINB, KU, FORM>;
+  auto kern = k_far_packed<KIND, M, MINB, KU, FORM, PAR>;
   BLTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = persistent_grid(kern, kWarps * 32, smem);
   kern<<<grid, kWarps * 32, smem, st>>>(a, it.items, it.n_items, it.poff, counter);
   BLTC_LAUNCH_CHECK();
+}
+
+template <int KIND>
+bool far_packed_dispatch_parity(const EvalArgs& a, const PackedItems& it, int* counter,
+                                cudaStream_t st) {
+  switch (a.degree + 1) {
+    case 5: far_packed_launch<KIND, 5, 1, 0, 2, true>(a, it, counter, st); return true;
+    case 6: far_packed_launch<KIND, 6, 1, 0, 2, true>(a, it, counter, st); return true;
+    case 8: far_packed_launch<KIND, 8, 1, 0, 2, true>(a, it, counter, st); return true;
+    case 9: far_packed_launch<KIND, 9, 1, 0, 2, true>(a, it, counter, st); return true;
+    case 11: far_packed_launch<KIND, 11, 1, 0, 2, true>(a, it, counter, st); return true;
+    default: return false;
+  }
 }
 
 template <int KIND>
@@ -668,11 +746,11 @@ bool far_packed_dispatch(const EvalArgs& a, const PackedItems& it, int* counter,
   }
 }
 
-template <int KIND, int CH = kNearCh, int FORM = 0>
+template <int KIND, int CH = kNearCh, int FORM = 0, bool PAR = false>
 void near_packed_launch(const EvalArgs& a, const PackedItems& it, int* counter,
                         cudaStream_t st) {
   const size_t smem = sizeof(double4) * kWarps * NearSmem<CH>::kWarp;
-  auto kern = k_near_packed<KIND, CH, 2, FORM>;
+  auto kern = k_near_packed<KIND, CH, 2, FORM, PAR>;
   BLTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = persistent_grid(kern, kWarps * 32, smem);
   kern<<<grid, kWarps * 32, smem, st>>>(a, it.items, it.n_items, it.poff, it.dmask, counter);
@@ -752,7 +830,8 @@ void build_packed_items(const EvalArgs& a, DBuf<int32_t>& pc, DBuf<int32_t>& pof
 }
 
 void launch_eval_packed(const EvalArgs& a, int kind, const PackedItems& it, int* counters,
-                        cudaStream_t st, float* far_ms, float* near_ms, bool timing) {
+                        cudaStream_t st, float* far_ms, float* near_ms, bool timing,
+                        bool parity) {
   if (a.nb == 0) return;
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
   if (timing) {
@@ -762,10 +841,19 @@ void launch_eval_packed(const EvalArgs& a, int kind, const PackedItems& it, int*
   }
   BLTC_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(int), st));
   if (timing) BLTC_CUDA(cudaEventRecord(e0, st));
-  if (kind == 0) far_packed_dispatch<0>(a, it, counters, st);
-  else far_packed_dispatch<1>(a, it, counters, st);
+  if (parity) {
+    if (kind == 0) far_packed_dispatch_parity<0>(a, it, counters, st);
+    else far_packed_dispatch_parity<1>(a, it, counters, st);
+  } else if (kind == 0) {
+    far_packed_dispatch<0>(a, it, counters, st);
+  } else {
+    far_packed_dispatch<1>(a, it, counters, st);
+  }
   if (timing) BLTC_CUDA(cudaEventRecord(e1, st));
-  if (tune_form() != 2) {
+  if (parity) {
+    if (kind == 0) near_packed_launch<0, kNearCh, 0, true>(a, it, counters + 1, st);
+    else near_packed_launch<1, kNearCh, 0, true>(a, it, counters + 1, st);
+  } else if (tune_form() != 2) {
     if (kind == 0) near_packed_launch<0>(a, it, counters + 1, st);
     else near_packed_launch<1>(a, it, counters + 1, st);
   } else {

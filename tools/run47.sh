@@ -1,0 +1,3 @@
+timeout 1200 python -m pytest tests -x -q -m gpu > gpurun_out/gpu_tests47.log 2>&1
+timeout 900 python bench.py --mode parity --steps 1 --no-accuracy --no-cpu-baseline > gpurun_out/b47_parity.json 2> gpurun_out/b47_parity.err
+timeout 900 python bench.py --config c2 --mode parity --steps 1 --no-accuracy --no-cpu-baseline > gpurun_out/b47_parity_c2.json 2> gpurun_out/b47_parity_c2.err
