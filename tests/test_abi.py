@@ -77,3 +77,19 @@ def test_cheb_nodes_match_reference_form():
     from paper_2003_01836_b200.engine import cheb_nodes
     for n in (0, 1, 2, 4, 8, 10, 13):
         np.testing.assert_array_equal(cheb_nodes(n), orc_nodes(n))
+
+
+def test_plain_c_host_compiles_and_links(tmp_path, lib):
+    """examples/treecode_c.c binds the C ABI with no Python / torch: the
+    header compiles as C and the program links against libbltc.so."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    libdir = os.path.join(ROOT, "paper_2003_01836_b200")
+    subprocess.run([gcc, "-std=c99", "-Wall", "-Werror", "-O2",
+                    f"-I{os.path.join(ROOT, 'include')}",
+                    os.path.join(ROOT, "examples", "treecode_c.c"), "-o",
+                    str(tmp_path / "treecode_c"), f"-L{libdir}", "-lbltc",
+                    f"-Wl,-rpath,{libdir}", "-lm"], check=True)
