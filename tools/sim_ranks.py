@@ -94,8 +94,9 @@ for R in map(int, args.ranks.split(",")):
         # per rank and phase, the minimum over repetitions (first-touch
         # allocations of the simulated ranks' buffers are not steady state)
         for r in range(R):
+            dm = mins.setdefault(r, {})
             for k, v in ph[r].items():
-                mins.setdefault(r, {})[k] = min(mins[r].get(k, v), v) if k != "pairs" else v
+                dm[k] = min(dm.get(k, v), v) if k != "pairs" else v
         ph = {r: dict(mins[r]) for r in range(R)}
         dev = {r: sum(ph[r][k] for k in ("build_ms", "publish_ms", "needs_ms", "let_host_ms",
                                            "evaluate_ms")) for r in range(R)}
