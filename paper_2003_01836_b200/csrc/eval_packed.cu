@@ -88,6 +88,17 @@ __device__ __forceinline__ double parity_term(double q, double d2, double kappa)
   return __ddiv_rn(__dmul_rn(exp(__dmul_rn(-kappa, r)), q), r);
 }
 
+// Coulomb PARITY term q / sqrt(d2) on the intrinsics' fast paths (bitwise
+// __ddiv_rn(q, __dsqrt_rn(d2)) when ok; 0 / s is exactly q for q = +-0).
+__device__ __forceinline__ double coulomb_parity_fp(double q, double d2, bool& ok) {
+  bool ok1, ok2;
+  const double sq = sqrt_rn_fastpath(d2, ok1);
+  const double t = div_rn_fastpath(q, sq, ok2);
+  const bool zero = q == 0.0;
+  ok = ok1 && (ok2 || zero);
+  return zero ? q : t;
+}
+
 __device__ __forceinline__ void neumaier(double& acc, double& comp, double t) {
   const double s = __dadd_rn(acc, t);
   const bool big = fabs(acc) >= fabs(t);
@@ -347,6 +358,7 @@ __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it
     far_stage_slab<M>(wsm, H, 0, lane);
     const bool act = e < mylen;
     double part[2] = {0.0, 0.0};
+    bool slow[2] = {false, false};   // PAR, Coulomb: an operand left the fast path
     __syncwarp();   // proxy points (plain stores) visible to the warp
     double dz2[2][M];
 #pragma unroll
@@ -389,12 +401,43 @@ __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
             const double d2 = __dadd_rn(dxy2[t], dz2[t][k3]);
-            if (PAR) part[t] = __dadd_rn(part[t], parity_term<KIND>(qv, d2, a.kappa));
-            else part[t] = pair_acc<KIND, FORM>(part[t], qv, d2, a.kappa);
+            if (PAR && KIND == 0) {
+              bool ok;
+              part[t] = __dadd_rn(part[t], coulomb_parity_fp(qv, d2, ok));
+              slow[t] |= !ok;
+            } else if (PAR) {
+              part[t] = __dadd_rn(part[t], parity_term<KIND>(qv, d2, a.kappa));
+            } else {
+              part[t] = pair_acc<KIND, FORM>(part[t], qv, d2, a.kappa);
+            }
           }
         }
       }
       __syncwarp();
+    }
+    if (PAR && KIND == 0 && __any_sync(0xffffffffu, slow[0] || slow[1])) {
+      // rare: redo this cluster's sum with the intrinsics (moments from the
+      // row in global memory -- the staged slabs are gone)
+      const double* row = H->row[L.g];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        if (!(slow[t] && act)) continue;
+        double p = 0.0;
+        int qi = 0;
+        for (int k1 = 0; k1 < M; ++k1) {
+          const double dx = __dsub_rn(tx[t], mpts[k1]);
+          for (int k2 = 0; k2 < M; ++k2) {
+            const double dy = __dsub_rn(ty[t], mpts[M + k2]);
+            const double dxy = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+            for (int k3 = 0; k3 < M; ++k3) {
+              const double dz = __dsub_rn(tz[t], mpts[2 * M + k3]);
+              const double d2 = __dadd_rn(dxy, __dmul_rn(dz, dz));
+              p = __dadd_rn(p, parity_term<KIND>(row[qi++], d2, a.kappa));
+            }
+          }
+        }
+        part[t] = p;
+      }
     }
 #pragma unroll
     for (int t = 0; t < 2; ++t) acc[t] = act ? __dadd_rn(acc[t], part[t]) : acc[t];
@@ -453,11 +496,14 @@ __device__ __forceinline__ void near_chunk(double (&part)[2], const double4* src
 // PARITY: the reference's _direct_tile pair by pair -- d2 unfused, pairs with
 // d2 < 1e-28 skipped, Neumaier into (acc, comp) (engine.py:166-213).  The
 // zero-charge padding records add +0 exactly (acc and comp are never -0).
-template <int KIND, int CH, bool MASKED>
+// FP: Coulomb terms on the intrinsics' fast paths; the caller replays the
+// chunk with FP = false for the (rare) lanes that report `slow`.
+template <int KIND, int CH, bool MASKED, bool FP = false>
 __device__ __forceinline__ void near_chunk_parity(double (&acc)[2], double (&comp)[2],
                                                   const double4* src, const double (&tx)[2],
                                                   const double (&ty)[2],
-                                                  const double (&tz)[2], double kappa) {
+                                                  const double (&tz)[2], double kappa,
+                                                  bool (&slow)[2]) {
   const long long tb = __double_as_longlong(kSingularSq);
 #pragma unroll 2
   for (int j = 0; j < CH; ++j) {
@@ -470,7 +516,14 @@ __device__ __forceinline__ void near_chunk_parity(double (&acc)[2], double (&com
       const double d2 =
           __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
       const bool ok = !MASKED || __double_as_longlong(d2) >= tb;
-      const double term = parity_term<KIND>(s.w, ok ? d2 : 1.0, kappa);
+      double term;
+      if (FP && KIND == 0) {
+        bool fast;
+        term = coulomb_parity_fp(s.w, ok ? d2 : 1.0, fast);
+        slow[t] |= ok && !fast;
+      } else {
+        term = parity_term<KIND>(s.w, ok ? d2 : 1.0, kappa);
+      }
       const double sum = __dadd_rn(acc[t], term);
       const bool big = fabs(acc[t]) >= fabs(term);
       const double hi = big ? acc[t] : term, lo = big ? term : acc[t];
@@ -634,10 +687,31 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
       }
       __syncwarp();
       if constexpr (PAR) {
+        const double acc0[2] = {acc[0], acc[1]}, comp0[2] = {comp[0], comp[1]};
+        bool slow[2] = {false, false};
         if (masked)
-          near_chunk_parity<KIND, CH, true>(acc, comp, mine + buf * CH, tx, ty, tz, a.kappa);
+          near_chunk_parity<KIND, CH, true, KIND == 0>(acc, comp, mine + buf * CH, tx, ty, tz,
+                                                       a.kappa, slow);
         else
-          near_chunk_parity<KIND, CH, false>(acc, comp, mine + buf * CH, tx, ty, tz, a.kappa);
+          near_chunk_parity<KIND, CH, false, KIND == 0>(acc, comp, mine + buf * CH, tx, ty, tz,
+                                                        a.kappa, slow);
+        if (KIND == 0 && __any_sync(0xffffffffu, slow[0] || slow[1])) {
+          // rare: replay the chunk with the intrinsics from its starting state
+          double acc1[2] = {acc0[0], acc0[1]}, comp1[2] = {comp0[0], comp0[1]};
+          bool unused[2] = {false, false};
+          if (masked)
+            near_chunk_parity<KIND, CH, true>(acc1, comp1, mine + buf * CH, tx, ty, tz,
+                                              a.kappa, unused);
+          else
+            near_chunk_parity<KIND, CH, false>(acc1, comp1, mine + buf * CH, tx, ty, tz,
+                                               a.kappa, unused);
+#pragma unroll
+          for (int t = 0; t < 2; ++t)
+            if (slow[t]) {
+              acc[t] = acc1[t];
+              comp[t] = comp1[t];
+            }
+        }
       } else {
         double part[2] = {0.0, 0.0};
         if (masked)
