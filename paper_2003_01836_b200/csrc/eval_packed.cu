@@ -466,12 +466,15 @@ struct NearSmem {
   static constexpr int kWarp = kGMax * kSeg;
 };
 
+#ifndef BLTC_NEAR_UNROLL
+#define BLTC_NEAR_UNROLL 4
+#endif
 template <int KIND, int CH, bool MASKED, int FORM>
 __device__ __forceinline__ void near_chunk(double (&part)[2], const double4* src,
                                            const double (&tx)[2], const double (&ty)[2],
                                            const double (&tz)[2], double kappa) {
   const long long tb = __double_as_longlong(kSingularSq);   // d2 >= 0: bit order = value order
-#pragma unroll 4
+#pragma unroll BLTC_NEAR_UNROLL
   for (int j = 0; j < CH; ++j) {
     const double4 s = src[j];
 #pragma unroll
