@@ -58,6 +58,14 @@ CONFIGS = {
                 n=8_000_000, kind=0, kappa=0.0, degree=8, theta=0.8, leaf=2000, batch=2000),
     "c5": dict(workload="C5: N=64M uniform cube, Coulomb, n=10, theta=0.7", gen="uniform",
                n=64_000_000, kind=0, kappa=0.0, degree=10, theta=0.7, leaf=2000, batch=1000),
+    # the paper's strong-scaling case (16.2 s on 32 P100)
+    "paper64m": dict(workload="64M uniform cube, Coulomb, n=8, theta=0.8, N_L=N_B=4000 "
+                              "(paper strong-scaling case)", gen="uniform", n=64_000_000,
+                     kind=0, kappa=0.0, degree=8, theta=0.8, leaf=4000, batch=4000),
+    "paper64m_y": dict(workload="64M uniform cube, Yukawa kappa=0.5, n=8, theta=0.8, "
+                                "N_L=N_B=4000 (paper strong-scaling case)", gen="uniform",
+                       n=64_000_000, kind=1, kappa=0.5, degree=8, theta=0.8, leaf=4000,
+                       batch=4000),
 }
 
 # Minimal FP64-pipe slots per pair: far / near field.
