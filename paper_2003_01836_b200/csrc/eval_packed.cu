@@ -469,12 +469,13 @@ struct NearSmem {
 #ifndef BLTC_NEAR_UNROLL
 #define BLTC_NEAR_UNROLL 4
 #endif
+constexpr int kNearUnroll = BLTC_NEAR_UNROLL;   // pragma arguments are not macro-expanded
 template <int KIND, int CH, bool MASKED, int FORM>
 __device__ __forceinline__ void near_chunk(double (&part)[2], const double4* src,
                                            const double (&tx)[2], const double (&ty)[2],
                                            const double (&tz)[2], double kappa) {
   const long long tb = __double_as_longlong(kSingularSq);   // d2 >= 0: bit order = value order
-#pragma unroll BLTC_NEAR_UNROLL
+#pragma unroll kNearUnroll
   for (int j = 0; j < CH; ++j) {
     const double4 s = src[j];
 #pragma unroll
