@@ -34,7 +34,7 @@ ctx = bltc.Context(0, stream.cuda_stream)
 envsets = [e for e in args.env.split("|")] if args.env else [""]
 for env in envsets:
     for kv in filter(None, env.split(";")):
-        k, v = kv.split("=")
+        k, v = kv.split("=", 1)
         os.environ[k] = v
     for leaf in map(int, args.leaf.split(",")):
         for batch in map(int, args.batch.split(",")):
