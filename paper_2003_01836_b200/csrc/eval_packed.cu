@@ -273,6 +273,7 @@ struct FarSmem {
   static constexpr int kSlab = M * M;
   static constexpr int kSeg = kPts + 2 * kSlab + 1;          // doubles per segment
   static constexpr int kWarp = kHdr + kGMax * kSeg + 1;      // doubles per warp
+  static constexpr int kDy = 2 * M * 32;                     // DY: dy^2 [M][2][32 lanes]
 };
 
 struct FarHdr {
@@ -301,10 +302,14 @@ __device__ __forceinline__ void far_stage_slab(double* wsm, const FarHdr* H, int
 // PAR: bitwise the reference's _approx_tile (per cluster a plain sum in k1,
 // k2, k3 order, then out += acc per cluster in list order): d2 unfused,
 // IEEE sqrt / division.
-template <int KIND, int M, int KU, int FORM, bool PAR = false>
+// DY: dy^2 per (target, k2) computed once per cluster into lane-private
+// shared-memory slots, so a row costs one DADD per target (dx^2 + dy^2)
+// instead of a DSUB and a DFMA.
+template <int KIND, int M, int KU, int FORM, bool PAR = false, bool DY = false>
 __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it,
                                                 const int32_t* poff, double* wsm, int lane) {
   using SM = FarSmem<M>;
+  double* dys = wsm + SM::kWarp + lane;   // DY slots: dys[(k2 * 2 + t) * 32]
   FarHdr* H = reinterpret_cast<FarHdr*>(wsm);
   const LaneTargets L = lane_targets(it, a, poff, lane);
   const double tx[2] = {a.tx[L.i0], a.tx[L.i1]};
@@ -370,6 +375,16 @@ __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it
         dz2[t][k3] = __dmul_rn(dz, dz);
       }
     }
+    if constexpr (DY) {
+      for (int k2 = 0; k2 < M; ++k2) {
+        const double p2 = mpts[M + k2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const double dy = __dsub_rn(ty[t], p2);
+          dys[(k2 * 2 + t) * 32] = __dmul_rn(dy, dy);
+        }
+      }
+    }
     for (int k1 = 0; k1 < M; ++k1) {
       if (k1 + 1 < M) {
         far_stage_slab<M>(wsm, H, k1 + 1, lane);
@@ -392,8 +407,12 @@ __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it
         double dxy2[2];
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
-          const double dy = __dsub_rn(ty[t], p2);
-          dxy2[t] = PAR ? __dadd_rn(dx2[t], __dmul_rn(dy, dy)) : fma(dy, dy, dx2[t]);
+          if constexpr (DY) {
+            dxy2[t] = __dadd_rn(dx2[t], dys[(k2 * 2 + t) * 32]);
+          } else {
+            const double dy = __dsub_rn(ty[t], p2);
+            dxy2[t] = PAR ? __dadd_rn(dx2[t], __dmul_rn(dy, dy)) : fma(dy, dy, dx2[t]);
+          }
         }
 #pragma unroll
         for (int k3 = 0; k3 < M; ++k3) {
@@ -446,15 +465,15 @@ __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it
   if (L.v1) a.far_out[L.i1] = acc[1];
 }
 
-template <int KIND, int M, int MINB, int KU, int FORM, bool PAR = false>
+template <int KIND, int M, int MINB, int KU, int FORM, bool PAR = false, bool DY = false>
 __global__ void __launch_bounds__(kWarps * 32, MINB)
 k_far_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int32_t* poff,
              int* counter) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* wsm = smem + warp * FarSmem<M>::kWarp;
+  double* wsm = smem + warp * (FarSmem<M>::kWarp + (DY ? FarSmem<M>::kDy : 0));
   for (int item = next_item(counter); item < n_items; item = next_item(counter))
-    far_packed_item<KIND, M, KU, FORM, PAR>(a, items[item], poff, wsm, lane);
+    far_packed_item<KIND, M, KU, FORM, PAR, DY>(a, items[item], poff, wsm, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -768,6 +787,10 @@ int tune_far_unroll(int kind) {
   // Coulomb: 3 rows per step, -2% far time at C4 (measured)
   return e ? std::atoi(e) : (kind == 0 ? 3 : 1);
 }
+int tune_far_dy() {
+  const char* e = std::getenv("BLTC_FAR_DY");
+  return e ? std::atoi(e) : 1;   // dy^2 per (target, k2) in shared memory: -0.7% far (measured)
+}
 int tune_form() {
   const char* e = std::getenv("BLTC_PFORM");
   return e ? std::atoi(e) : 2;   // FORM 2: -0.9% far, -1.5% near at C4 (measured)
@@ -783,10 +806,12 @@ int persistent_grid(K kernel, int threads, size_t smem) {
   return sms * (per_sm > 0 ? per_sm : 1);
 }
 
-template <int KIND, int M, int KU = 1, int FORM = 0, int MINB = 2, bool PAR = false>
+template <int KIND, int M, int KU = 1, int FORM = 0, int MINB = 2, bool PAR = false,
+          bool DY = false>
 void far_packed_launch(const EvalArgs& a, const PackedItems& it, int* counter, cudaStream_t st) {
-  const size_t smem = sizeof(double) * kWarps * FarSmem<M>::kWarp;
-  auto kern = k_far_packed<KIND, M, MINB, KU, FORM, PAR>;
+  const size_t smem =
+      sizeof(double) * kWarps * (FarSmem<M>::kWarp + (DY ? FarSmem<M>::kDy : 0));
+  auto kern = k_far_packed<KIND, M, MINB, KU, FORM, PAR, DY>;
   BLTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = persistent_grid(kern, kWarps * 32, smem);
   kern<<<grid, kWarps * 32, smem, st>>>(a, it.items, it.n_items, it.poff, counter);
@@ -816,6 +841,8 @@ bool far_packed_dispatch(const EvalArgs& a, const PackedItems& it, int* counter,
     case 9:
       // tuned for the benchmark degree: k2 unrolled by 3, FORM 2 (measured)
       if (tune_form() != 2) far_packed_launch<KIND, 9, 1, 0>(a, it, counter, st);
+      else if (KIND == 0 && tune_far_dy())
+        far_packed_launch<KIND, 9, 3, 2, 2, false, true>(a, it, counter, st);
       else if (tune_far_unroll(KIND) == 3) far_packed_launch<KIND, 9, 3, 2>(a, it, counter, st);
       else far_packed_launch<KIND, 9, 1, 2>(a, it, counter, st);
       return true;
