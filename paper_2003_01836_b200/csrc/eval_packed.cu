@@ -23,8 +23,13 @@
 //     staged kNearCh packed (x, y, z, q) records at a time (double-
 //     buffered); exhausted streams are padded with zero-charge records far
 //     away, which add exactly 0.
-// The per-pair arithmetic is eval_fast.cu's (rsqrt seed + cubic correction,
-// 7 / 12 FP64 slots per far / near pair).
+// FAST arithmetic: rsqrt seed + cubic correction, the charge / moment as the
+// operand a lane's two targets share (FORM 2), 7 / 12 FP64 slots per far /
+// near pair; Yukawa with the table-driven exp (eval_common.cuh).  PAR: the
+// same items and staging with the reference's arithmetic and order, bitwise
+// (one source group; the distributed forest uses eval_parity.cu).
+// Measured choices: kGMax = 4, two targets per lane, 8 warps x
+// 2 CTAs per SM (register bound), k2 unrolled by 3, dy^2 in shared memory.
 #include "bltc_internal.cuh"
 #include "eval_common.cuh"
 
