@@ -132,6 +132,60 @@ def rcb_partition(points: Points, ranks: int) -> RcbPartition:
                         regions=regions, cuts=cuts)
 
 
+class DeviceRcb:
+    """RCB on the device (FAST runs): the same cuts, axes and per-rank counts
+    as rcb_partition (decomp.py:76-130) -- exact order statistics, floor/ceil
+    shares, the longest slab extent, ties to the lowest axis -- but each cut
+    is a stable device sort instead of numpy's argpartition, so the order of
+    particles WITHIN a rank differs from the reference's (tree shapes and
+    cluster memberships do not; only summation order in FAST sums does).
+    ``order`` stays on the device."""
+
+    def __init__(self, x, y, z, ranks: int):
+        import torch
+        n = int(x.numel())
+        if ranks < 1:
+            raise ValueError("ranks must be >= 1")
+        if n < ranks:
+            raise ValueError(f"need at least one particle per rank ({n} < {ranks})")
+        coords = (x, y, z)
+        lo = np.array([float(c.min().item()) for c in coords])
+        hi = np.array([float(c.max().item()) for c in coords])
+        self.order = torch.arange(n, device=x.device)
+        shares = np.array([(n * (r + 1)) // ranks - (n * r) // ranks for r in range(ranks)],
+                          dtype=np.int64)
+        self.rank_start = np.concatenate(([0], np.cumsum(shares)))
+
+        def recurse(start, stop, r0, r1, lo, hi):
+            if r1 - r0 == 1:
+                return
+            rm = r0 + (r1 - r0) // 2
+            n_left = int(shares[r0:rm].sum())
+            axis = _cut_axis(lo, hi)
+            idx = self.order[start:stop]
+            vals = coords[axis][idx]
+            perm = torch.argsort(vals, stable=True)
+            self.order[start:stop] = idx[perm]
+            sv = vals[perm]
+            left_max, right_min = (float(v) for v in sv[[n_left - 1, n_left]].tolist())
+            cut = 0.5 * (left_max + right_min)
+            lo_hi = hi.copy()
+            lo_hi[axis] = cut
+            hi_lo = lo.copy()
+            hi_lo[axis] = cut
+            recurse(start, start + n_left, r0, rm, lo, lo_hi)
+            recurse(start + n_left, stop, rm, r1, hi_lo, hi)
+
+        recurse(0, n, 0, ranks, lo, hi)
+
+    def rank_indices(self, rank: int):
+        return self.order[int(self.rank_start[rank]):int(self.rank_start[rank + 1])]
+
+    @property
+    def counts(self) -> np.ndarray:
+        return np.diff(self.rank_start)
+
+
 # ---------------------------------------------------------------------------
 # Published rank data and its exchange
 
@@ -612,22 +666,32 @@ def _process_group_world(group):
 
 
 def run_distributed(system, config, ranks: int, threads: int = 1, mode: str | None = None,
-                    group=None, engine_factory=None, exchange: str = "let"):
+                    group=None, engine_factory=None, exchange: str = "let",
+                    partition: str = "auto"):
     """decomp.py:483-593 on GPUs.  Returns (phi in original order, stats) on
     every participating process.  ``threads`` is accepted and ignored;
-    ``exchange`` is "let" (the reference's minimal fetch) or "replicate"."""
+    ``exchange`` is "let" (the reference's minimal fetch) or "replicate";
+    ``partition`` "host" is the reference's numpy RCB (its exact particle
+    order, needed for bitwise PARITY), "device" the same cuts on the GPU
+    (DeviceRcb), "auto" = device for FAST runs on the device engine."""
     import time
 
     import torch
 
+    from .engine import DEFAULT_MODE
+
     del threads
     if exchange not in ("let", "replicate"):
         raise ValueError(f"exchange must be 'let' or 'replicate', got {exchange!r}")
+    if partition not in ("auto", "host", "device"):
+        raise ValueError(f"partition must be 'auto', 'host' or 'device', got {partition!r}")
     if not system.coincident:
         raise ValueError("distributed runs require targets and sources "
                          "to be the same particle set")
     t_start = time.perf_counter()
-    part = rcb_partition(system.sources, ranks)
+    resolved = DEFAULT_MODE if mode is None else mode
+    on_device = partition == "device" or (partition == "auto" and engine_factory is None
+                                          and resolved == "fast")
     dist, world, me = _process_group_world(group)
     if world > 1 and world != ranks:
         raise ValueError(f"ranks ({ranks}) must equal the process-group size ({world})")
@@ -637,6 +701,13 @@ def run_distributed(system, config, ranks: int, threads: int = 1, mode: str | No
     src = system.sources
     x, y, z = np.asarray(src.x), np.asarray(src.y), np.asarray(src.z)
     q = np.asarray(system.charges)
+    if on_device:
+        dev = torch.device("cuda", torch.cuda.current_device())
+        x, y, z, q = (torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(dev)
+                      for v in (x, y, z, q))
+        part = DeviceRcb(x, y, z, ranks)
+    else:
+        part = rcb_partition(system.sources, ranks)
     timings = {}
     t0 = time.perf_counter()
     for r in mine:
@@ -684,14 +755,18 @@ def run_distributed(system, config, ranks: int, threads: int = 1, mode: str | No
         buf[:mine_phi.numel()] = mine_phi
         gathered = [torch.empty_like(buf) for _ in range(ranks)]
         _all_gather(gathered, buf, group=group)
-        for o in range(ranks):
-            phi[part.rank_indices(o)] = gathered[o][:counts[o]].cpu().numpy()
+        rank_phi = {o: gathered[o][:counts[o]] for o in range(ranks)}
         tot = torch.tensor(local, dtype=torch.int64, device=dev)
         _all_reduce(tot, group=group)
         local = tot.cpu().numpy()
+    if on_device:
+        full = torch.empty(len(system.targets), dtype=torch.float64, device=x.device)
+        for o in range(ranks):
+            full[part.rank_indices(o)] = rank_phi[o].reshape(-1).to(x.device)
+        phi = full.cpu().numpy()
     else:
         for o in range(ranks):
-            phi[part.rank_indices(o)] = rank_phi[o].detach().cpu().numpy()
+            phi[part.rank_indices(o)] = rank_phi[o].detach().reshape(-1).cpu().numpy()
     if exchange == "replicate":
         for r in mine:
             for o in range(ranks):

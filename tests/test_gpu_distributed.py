@@ -89,3 +89,34 @@ def test_let_exchange_matches_reference_fetch(bltc, case):
                       for (o, w), f in sorted(st_l.fetch_stats.items())], dtype=np.int64)
     np.testing.assert_array_equal(fetch, g["fetch"])
     assert (st_l.direct_pairs, st_l.approx_pairs) == (st_r.direct_pairs, st_r.approx_pairs)
+
+
+@pytest.mark.parametrize("ranks", [2, 3, 8])
+def test_device_rcb_same_rank_sets(bltc, ranks):
+    """RCB on the device: the reference's cuts -- every rank receives the same
+    particle set (and count) as numpy's rcb_partition, only the order within
+    a rank differs."""
+    import torch
+    from paper_2003_01836_b200 import cli
+    from paper_2003_01836_b200.decomp import DeviceRcb, rcb_partition
+    s = cli.generate_plummer(50_000, 21)
+    src = s.sources
+    host = rcb_partition(src, ranks)
+    dev = torch.device("cuda", 0)
+    d = DeviceRcb(*(torch.from_numpy(np.asarray(v)).to(dev) for v in (src.x, src.y, src.z)),
+                  ranks)
+    np.testing.assert_array_equal(d.counts, host.counts)
+    for r in range(ranks):
+        np.testing.assert_array_equal(np.sort(d.rank_indices(r).cpu().numpy()),
+                                      np.sort(host.rank_indices(r)))
+
+
+def test_fast_device_partition_matches_reference(bltc):
+    from paper_2003_01836_b200.decomp import run_distributed
+    g = golden("dist_r4_yukawa")
+    s = golden_system(g)
+    phi, st = run_distributed(s, _cfg(bltc, g), ranks=int(g["ranks"]), mode="fast",
+                              partition="device")
+    _check(phi, g["phi"], False, 1e-13)
+    assert (st.direct_pairs, st.approx_pairs) == (int(g["direct_pairs"]),
+                                                  int(g["approx_pairs"]))
