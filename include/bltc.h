@@ -142,6 +142,20 @@ BLTC_API int bltc_export_lists(bltc_ctx* ctx, int64_t* a_ptr, int64_t* a_idx, in
 /* Moments: cluster ids [n_moments] and rows [n_moments][(n+1)^3]. */
 BLTC_API int bltc_export_moments(bltc_ctx* ctx, int64_t* cluster_ids, double* rows);
 
+/* run_distributed (decomp.py:483-593) in one process: R ranks on the given
+ * devices (rank r on devices[r % n_devices]), one host thread per rank; the
+ * caller's RCB (rcb_order / rank_start, e.g. the reference's rcb_partition)
+ * decides each rank's particles and their order.  Ranks evaluate against
+ * every rank's published buffers across devices (peer access where
+ * available) in the reference's owner order.  Host pointers; phi_out in the
+ * original order; stats: sums of the pair counts, max of the times. */
+BLTC_API int bltc_run_distributed(int32_t ranks, const int32_t* devices, int32_t n_devices,
+                                  const bltc_params* p, const double* cheb_s, int64_t n,
+                                  const double* x, const double* y, const double* z,
+                                  const double* q, const int64_t* rcb_order,
+                                  const int64_t* rank_start, double* phi_out,
+                                  bltc_stats* stats);
+
 /* ---- Stage calls with host-provided upstream structures -------------------
  * Each stage of the pipeline on structures the caller built (e.g. the
  * reference's own tree / batches / lists / moments, flattened), so a stage
@@ -208,7 +222,7 @@ BLTC_API int bltc_rank_build(bltc_ctx* ctx, const bltc_params* p, const double* 
                     int32_t device_ptrs);
 BLTC_API int bltc_rank_publish_sizes(bltc_ctx* ctx, bltc_publish_sizes* out);
 /* records: [n_clusters][record_doubles]; particles: [4][n_particles] (x,y,z,q);
- * moments: [n_moment_rows][(n+1)^3].  All device pointers. */
+ * moments: [n_moment_rows][(n+1)^3 rounded up to even].  All device pointers. */
 BLTC_API int bltc_rank_publish(bltc_ctx* ctx, double* records, double* particles, double* moments);
 /* Forest of R published trees (device pointers, one per owner rank, owner
  * order 0..R-1); my_rank's own entry is the local tree.  phi_out: host (or

@@ -91,6 +91,10 @@ SIGNATURES = {
                                        ctypes.c_int32, _i64p, ctypes.POINTER(_vp), _vp]),
     "bltc_probe_fp64": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _f64p]),
     "bltc_launch_count": (ctypes.c_int, [_i64p]),
+    "bltc_run_distributed": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                                            ctypes.c_int32, ctypes.POINTER(Params), _f64p,
+                                            ctypes.c_int64, _f64p, _f64p, _f64p, _f64p, _i64p,
+                                            _i64p, _f64p, ctypes.POINTER(Stats)]),
     "bltc_philox_uniform": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_uint64),
                                            ctypes.POINTER(ctypes.c_uint64), ctypes.c_int64,
                                            ctypes.c_int32, ctypes.c_double, ctypes.c_double,

@@ -821,3 +821,53 @@ class DeviceRankRunner:
             forest = all_gather_published(pub, self.ranks, self.group)
         self.phi = self.engine.evaluate(self.ranks, self.me, forest)
         return self.engine.stats
+
+
+def run_distributed_native(system, config, ranks: int, devices=None, mode: str | None = None):
+    """run_distributed (decomp.py:483-593) through the single C call
+    ``bltc_run_distributed``: R ranks in this process on ``devices`` (rank r
+    on devices[r % len(devices)], default: every visible GPU), the
+    reference's host RCB (rcb_partition) fixing each rank's particles and
+    order.  No torch.distributed; ranks read each other's published trees
+    across devices.  Returns (phi in original order, DistributedStats)."""
+    import ctypes
+    import time
+
+    from . import _lib
+    from .engine import cheb_nodes, make_params
+
+    if not system.coincident:
+        raise ValueError("distributed runs require targets and sources "
+                         "to be the same particle set")
+    if ranks < 1:
+        raise ValueError("ranks must be >= 1")
+    if devices is None:
+        import torch
+        devices = list(range(max(1, torch.cuda.device_count())))
+    devices = np.ascontiguousarray(devices, dtype=np.int32)
+    t0 = time.perf_counter()
+    src = system.sources
+    part = rcb_partition(src, ranks)
+    counts = np.diff(part.rank_start)
+    if (counts < 1).any():
+        raise ValueError("every rank needs at least one particle")
+    p = make_params(config, mode)
+    s = cheb_nodes(int(config.degree))
+    f64 = lambda a: np.ascontiguousarray(a, dtype=np.float64)
+    x, y, z, q = f64(src.x), f64(src.y), f64(src.z), f64(system.charges)
+    order = np.ascontiguousarray(part.order, dtype=np.int64)
+    start = np.ascontiguousarray(part.rank_start, dtype=np.int64)
+    n = len(x)
+    phi = np.empty(n)
+    st = _lib.Stats()
+    dp = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    ip = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+    _lib.check(_lib.load().bltc_run_distributed(
+        ranks, devices.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), len(devices),
+        ctypes.byref(p), dp(s), n, dp(x), dp(y), dp(z), dp(q), ip(order), ip(start), dp(phi),
+        ctypes.byref(st)))
+    return phi, DistributedStats(
+        n_ranks=ranks, rank_counts=counts, n_clusters=int(st.n_clusters),
+        n_batches=int(st.n_batches), direct_pairs=int(st.direct_pairs),
+        approx_pairs=int(st.approx_pairs), setup_s=float(st.setup_s),
+        compute_s=float(st.compute_s), total_s=time.perf_counter() - t0)

@@ -120,3 +120,51 @@ def test_fast_device_partition_matches_reference(bltc):
     _check(phi, g["phi"], False, 1e-13)
     assert (st.direct_pairs, st.approx_pairs) == (int(g["direct_pairs"]),
                                                   int(g["approx_pairs"]))
+
+
+@pytest.mark.parametrize("case", ["dist_r3", "dist_r4_yukawa"])
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+def test_c_run_distributed_matches_reference(bltc, case, mode):
+    """bltc_run_distributed (one C call, one host thread per rank) reproduces
+    the reference's run_distributed: PARITY bitwise for Coulomb."""
+    from paper_2003_01836_b200.decomp import run_distributed_native
+    g = golden(case)
+    s = golden_system(g)
+    phi, st = run_distributed_native(s, _cfg(bltc, g), ranks=int(g["ranks"]), devices=[0],
+                                     mode=mode)
+    exact = mode == "parity" and int(g["kind"]) == 0
+    _check(phi, g["phi"], exact, 1e-14 if mode == "parity" else 1e-13)
+    assert st.direct_pairs == int(g["direct_pairs"])
+    assert st.approx_pairs == int(g["approx_pairs"])
+    np.testing.assert_array_equal(st.rank_counts, np.diff(g["rank_start"]))
+
+
+def test_c_run_distributed_plummer_vs_python_path(bltc):
+    from paper_2003_01836_b200 import cli
+    from paper_2003_01836_b200.decomp import run_distributed, run_distributed_native
+    s = cli.generate_plummer(60_000, 9)
+    cfg = bltc.EvalConfig(theta=0.8, degree=6, leaf_size=500, batch_size=500)
+    a, sa = run_distributed(s, cfg, ranks=4, mode="parity")
+    b, sb = run_distributed_native(s, cfg, ranks=4, devices=[0], mode="parity")
+    np.testing.assert_array_equal(a, b)
+    assert (sa.direct_pairs, sa.approx_pairs) == (sb.direct_pairs, sb.approx_pairs)
+
+
+def test_c_run_distributed_rejects_bad_partition(bltc):
+    import ctypes
+    from paper_2003_01836_b200 import _lib, cli
+    from paper_2003_01836_b200.engine import cheb_nodes, make_params
+    s = cli.generate_particles(100, 1)
+    cfg = bltc.EvalConfig(theta=0.8, degree=2, leaf_size=10, batch_size=10)
+    p = make_params(cfg)
+    x = np.ascontiguousarray(s.sources.x)
+    dp = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    ip = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+    order = np.arange(100, dtype=np.int64)
+    start = np.array([0, 60, 90], dtype=np.int64)        # does not end at n
+    dev = np.zeros(1, np.int32)
+    phi = np.empty(100)
+    rc = _lib.load().bltc_run_distributed(
+        2, dev.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), 1, ctypes.byref(p),
+        dp(cheb_nodes(2)), 100, dp(x), dp(x), dp(x), dp(x), ip(order), ip(start), dp(phi), None)
+    assert rc == -1
