@@ -501,7 +501,8 @@ def run_ours(args, cfg):
         "pairs": {"approx": st.approx_pairs, "direct": st.direct_pairs,
                   "clusters": st.n_clusters, "batches": st.n_batches,
                   "moments": st.n_moments},
-        "roofline": {"bound": "fp64", "kernel": "k_far_fast (far field)",
+        "roofline": {"bound": "fp64",
+                     "kernel": ("k_far_packed" if getattr(st, "packed", 0) else "k_far_fast") + " (far field)",
                      "achieved": far_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": far_tflops / peak_tflops if peak_tflops else None,
                      "traffic": traffic,
@@ -510,7 +511,8 @@ def run_ours(args, cfg):
                                     "sustained ~0.3 s)",
                      "peak_nominal": nominal_tflops,
                      "frac_nominal": far_tflops / nominal_tflops if nominal_tflops else None},
-        "near_roofline": {"kernel": "k_near_fast (near field)", "achieved": near_tflops,
+        "near_roofline": {"kernel": ("k_near_packed" if getattr(st, "packed", 0) else "k_near_fast")
+                                     + " (near field)", "achieved": near_tflops,
                           "frac": near_tflops / peak_tflops if peak_tflops else None,
                           "work": f"{s_near} FP64 slots/pair x direct pairs"},
         "interaction_frac": ((2.0 * (s_far * st.approx_pairs + s_near * st.direct_pairs)
