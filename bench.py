@@ -70,9 +70,10 @@ CONFIGS = {
 
 # Minimal FP64-pipe slots per pair: far / near field.
 # Yukawa: SURVEY.md counts libdevice exp as 15 slots (25 / 30); the kernels
-# use a 10-slot table-driven exp (eval_common.cuh exp_neg_fast), so the
-# algorithmic count here is the lower 20 / 25 (the roofline is not inflated).
-SLOTS = {0: (7, 12), 1: (20, 25), 2: (1, 1)}
+# fold kappa into a table-driven exp of 8 slots (eval_common.cuh exp_neg_kr),
+# so the algorithmic count here is the lower 17 / 22 (the roofline is not
+# inflated).
+SLOTS = {0: (7, 12), 1: (17, 22), 2: (1, 1)}
 
 
 def log(*a):

@@ -511,6 +511,7 @@ void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, 
   a.s_nodes = c->s_nodes.p;
   a.degree = p->degree;
   a.kappa = p->kappa;
+  a.yk = make_yukawa_k(p->kappa);
   c->out_sorted.resize(T.n);
   a.out = c->out_sorted.p;
   const bool parity_packed = p->mode == BLTC_MODE_PARITY && G == 1 &&

@@ -84,12 +84,12 @@ __device__ __forceinline__ double coulomb_acc(double acc, double q, double d2) {
 }
 
 template <int KIND, int FORM>
-__device__ __forceinline__ double pair_acc(double acc, double q, double d2, double kappa) {
+__device__ __forceinline__ double pair_acc(double acc, double q, double d2, const YukawaK& yk) {
   if (KIND == 0) return coulomb_acc<FORM>(acc, q, d2);
   if (KIND == 1) {
     const double y = rsqrt_fast(d2);
     const double r = __dmul_rn(d2, y);
-    return fma(__dmul_rn(q, exp_neg_fast(-__dmul_rn(kappa, r))), y, acc);
+    return fma(__dmul_rn(q, exp_neg_kr(r, yk)), y, acc);
   }
   return __dadd_rn(acc, q);
 }
@@ -98,13 +98,13 @@ __device__ __forceinline__ double pair_acc(double acc, double q, double d2, doub
 template <int KIND, int M, int kTpt, int FORM>
 __device__ __forceinline__ void far_row(double (&acc)[kTpt], const double* qr,
                                         const double (&dxy2)[kTpt],
-                                        const double (&dz2)[kTpt][M], double kappa) {
+                                        const double (&dz2)[kTpt][M], const YukawaK& yk) {
 #pragma unroll
   for (int k3 = 0; k3 < M; ++k3) {
     const double qv = qr[k3];
 #pragma unroll
     for (int k = 0; k < kTpt; ++k)
-      acc[k] = pair_acc<KIND, FORM>(acc[k], qv, __dadd_rn(dxy2[k], dz2[k][k3]), kappa);
+      acc[k] = pair_acc<KIND, FORM>(acc[k], qv, __dadd_rn(dxy2[k], dz2[k][k3]), yk);
   }
 }
 
@@ -175,7 +175,7 @@ __device__ __forceinline__ void far_item(const EvalArgs& a, int b, int t0, int t
               const double dy = __dsub_rn(ty[k], p2);
               dxy2[k] = fma(dy, dy, dx2[k]);
             }
-            far_row<KIND, M, kTpt, FORM>(acc, qr, dxy2, dz2, a.kappa);
+            far_row<KIND, M, kTpt, FORM>(acc, qr, dxy2, dz2, a.yk);
           }
         }
       } else {
@@ -197,7 +197,7 @@ __device__ __forceinline__ void far_item(const EvalArgs& a, int b, int t0, int t
 #pragma unroll
               for (int k = 0; k < kTpt; ++k) {
                 const double dz = __dsub_rn(tz[k], p3);
-                acc[k] = pair_acc<KIND, FORM>(acc[k], qv, fma(dz, dz, dxy2[k]), a.kappa);
+                acc[k] = pair_acc<KIND, FORM>(acc[k], qv, fma(dz, dz, dxy2[k]), a.yk);
               }
             }
           }
@@ -266,7 +266,7 @@ __device__ __forceinline__ double ball_box_gap(const double* bc, double br, cons
 template <int KIND, int kTpt, int FORM, bool MASKED>
 __device__ __forceinline__ void near_chunk(double (&part)[kTpt], const double4* src, int jn,
                                            const double (&tx)[kTpt], const double (&ty)[kTpt],
-                                           const double (&tz)[kTpt], double kappa) {
+                                           const double (&tz)[kTpt], const YukawaK& yk) {
   const long long tb = __double_as_longlong(kSingularSq);   // d2 >= 0: bit order = value order
 #pragma unroll 4
   for (int j = 0; j < jn; ++j) {
@@ -281,10 +281,10 @@ __device__ __forceinline__ void near_chunk(double (&part)[kTpt], const double4* 
         // only the charge needs the select (excluded pairs add 0 * finite)
         const double d2 = fma(dz, dz, fma(dy, dy, fma(dx, dx, 1e-300)));
         const bool ok = __double_as_longlong(d2) >= tb;
-        part[k] = pair_acc<KIND, FORM>(part[k], ok ? s.w : 0.0, d2, kappa);
+        part[k] = pair_acc<KIND, FORM>(part[k], ok ? s.w : 0.0, d2, yk);
       } else {
         const double d2 = fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx)));
-        part[k] = pair_acc<KIND, FORM>(part[k], s.w, d2, kappa);
+        part[k] = pair_acc<KIND, FORM>(part[k], s.w, d2, yk);
       }
     }
   }
@@ -330,9 +330,9 @@ __device__ __forceinline__ void near_item(const EvalArgs& a, int b, int t0, int 
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) part[k] = 0.0;
         if (masked)
-          near_chunk<KIND, kTpt, FORM, true>(part, stage[buf], jn, tx, ty, tz, a.kappa);
+          near_chunk<KIND, kTpt, FORM, true>(part, stage[buf], jn, tx, ty, tz, a.yk);
         else
-          near_chunk<KIND, kTpt, FORM, false>(part, stage[buf], jn, tx, ty, tz, a.kappa);
+          near_chunk<KIND, kTpt, FORM, false>(part, stage[buf], jn, tx, ty, tz, a.yk);
 #pragma unroll
         for (int k = 0; k < kTpt; ++k) neumaier(acc[k], comp[k], part[k]);
         __syncwarp();

@@ -75,11 +75,11 @@ __device__ __forceinline__ double coulomb_acc(double acc, double q, double d2) {
 }
 
 template <int KIND, int FORM = 0>
-__device__ __forceinline__ double pair_acc(double acc, double q, double d2, double kappa) {
+__device__ __forceinline__ double pair_acc(double acc, double q, double d2, const YukawaK& yk) {
   if (KIND == 0) return coulomb_acc<FORM>(acc, q, d2);
   const double y = rsqrt_fast(d2);
   const double r = __dmul_rn(d2, y);
-  const double ex = exp_neg_fast(-__dmul_rn(kappa, r));
+  const double ex = exp_neg_kr(r, yk);
   if (FORM == 2) return fma(q, __dmul_rn(ex, y), acc);
   return fma(__dmul_rn(q, ex), y, acc);
 }
@@ -432,7 +432,7 @@ __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it
             } else if (PAR) {
               part[t] = __dadd_rn(part[t], parity_term<KIND>(qv, d2, a.kappa));
             } else {
-              part[t] = pair_acc<KIND, FORM>(part[t], qv, d2, a.kappa);
+              part[t] = pair_acc<KIND, FORM>(part[t], qv, d2, a.yk);
             }
           }
         }
@@ -497,7 +497,7 @@ constexpr int kNearUnroll = BLTC_NEAR_UNROLL;   // pragma arguments are not macr
 template <int KIND, int CH, bool MASKED, int FORM>
 __device__ __forceinline__ void near_chunk(double (&part)[2], const double4* src,
                                            const double (&tx)[2], const double (&ty)[2],
-                                           const double (&tz)[2], double kappa) {
+                                           const double (&tz)[2], const YukawaK& yk) {
   const long long tb = __double_as_longlong(kSingularSq);   // d2 >= 0: bit order = value order
 #pragma unroll kNearUnroll
   for (int j = 0; j < CH; ++j) {
@@ -512,10 +512,10 @@ __device__ __forceinline__ void near_chunk(double (&part)[2], const double4* src
         // only the charge needs the select (excluded pairs add 0 * finite)
         const double d2 = fma(dz, dz, fma(dy, dy, fma(dx, dx, 1e-300)));
         const bool ok = __double_as_longlong(d2) >= tb;
-        part[t] = pair_acc<KIND, FORM>(part[t], ok ? s.w : 0.0, d2, kappa);
+        part[t] = pair_acc<KIND, FORM>(part[t], ok ? s.w : 0.0, d2, yk);
       } else {
         const double d2 = fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx)));
-        part[t] = pair_acc<KIND, FORM>(part[t], s.w, d2, kappa);
+        part[t] = pair_acc<KIND, FORM>(part[t], s.w, d2, yk);
       }
     }
   }
@@ -743,9 +743,9 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
       } else {
         double part[2] = {0.0, 0.0};
         if (masked)
-          near_chunk<KIND, CH, true, FORM>(part, mine + buf * CH, tx, ty, tz, a.kappa);
+          near_chunk<KIND, CH, true, FORM>(part, mine + buf * CH, tx, ty, tz, a.yk);
         else
-          near_chunk<KIND, CH, false, FORM>(part, mine + buf * CH, tx, ty, tz, a.kappa);
+          near_chunk<KIND, CH, false, FORM>(part, mine + buf * CH, tx, ty, tz, a.yk);
 #pragma unroll
         for (int t = 0; t < 2; ++t) neumaier(acc[t], comp[t], part[t]);
       }
