@@ -8,13 +8,21 @@
  * Uniform random particles in [-1,1]^3 (an LCG, not the harness's Philox
  * stream), Coulomb, n = 6, theta = 0.7: the treecode potentials in PARITY
  * and FAST mode, checked against a brute-force direct sum on a sample of
- * targets (relative L2 error, cli.py:152-159) and against each other. */
+ * targets (relative L2 error, cli.py:152-159) and against each other; then
+ * a 2-rank bltc_run_distributed over a median split in x (any partition the
+ * caller chooses; decomp.rcb_partition's is the reference's). */
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
 
 #include "bltc.h"
+
+static const double* sort_key;
+static int by_key(const void* a, const void* b) {
+  const double u = sort_key[*(const int64_t*)a], v = sort_key[*(const int64_t*)b];
+  return (u > v) - (u < v);
+}
 
 static uint64_t lcg = 0x9E3779B97F4A7C15ull;
 static double uniform(void) {
@@ -36,6 +44,8 @@ int main(int argc, char** argv) {
   double *x = malloc(n * sizeof(double)), *y = malloc(n * sizeof(double));
   double *z = malloc(n * sizeof(double)), *q = malloc(n * sizeof(double));
   double *phi_p = malloc(n * sizeof(double)), *phi_f = malloc(n * sizeof(double));
+  double* phi_d = malloc(n * sizeof(double));
+  int64_t* order = malloc(n * sizeof(int64_t));
   for (int64_t i = 0; i < n; ++i) {
     x[i] = uniform();
     y[i] = uniform();
@@ -60,8 +70,17 @@ int main(int argc, char** argv) {
     return 1;
   }
   CHECK(bltc_destroy(ctx));
+  /* two ranks: lower / upper half in x, both on device 0 */
+  for (int64_t i = 0; i < n; ++i) order[i] = i;
+  sort_key = x;
+  qsort(order, (size_t)n, sizeof(int64_t), by_key);
+  const int64_t rank_start[3] = {0, n / 2, n};
+  const int32_t devices[1] = {0};
+  bltc_stats dst;
+  CHECK(bltc_run_distributed(2, devices, 1, &p, s, n, x, y, z, q, order, rank_start, phi_d,
+                             &dst));
   /* direct sum on every 97th target, Neumaier-compensated */
-  double num = 0.0, den = 0.0, dev = 0.0, scale = 0.0;
+  double num = 0.0, den = 0.0, numd = 0.0, dev = 0.0, scale = 0.0;
   for (int64_t i = 0; i < n; i += 97) {
     double acc = 0.0, comp = 0.0;
     for (int64_t j = 0; j < n; ++j) {
@@ -74,15 +93,16 @@ int main(int argc, char** argv) {
     }
     const double ds = acc + comp;
     num += (phi_p[i] - ds) * (phi_p[i] - ds);
+    numd += (phi_d[i] - ds) * (phi_d[i] - ds);
     den += ds * ds;
   }
   for (int64_t i = 0; i < n; ++i) {
     dev = fmax(dev, fabs(phi_f[i] - phi_p[i]));
     scale = fmax(scale, fabs(phi_p[i]));
   }
-  const double err = sqrt(num / den), rel = dev / scale;
+  const double err = sqrt(num / den), errd = sqrt(numd / den), rel = dev / scale;
   printf("{\"n\": %lld, \"clusters\": %lld, \"batches\": %lld, \"rel_l2_error\": %.3e, "
-         "\"fast_vs_parity\": %.3e}\n", (long long)n, (long long)st.n_clusters,
-         (long long)st.n_batches, err, rel);
-  return (err < 1e-4 && rel < 1e-13) ? 0 : 2;
+         "\"fast_vs_parity\": %.3e, \"ranks2_rel_l2_error\": %.3e}\n", (long long)n,
+         (long long)st.n_clusters, (long long)st.n_batches, err, rel, errd);
+  return (err < 1e-4 && rel < 1e-13 && errd < 1e-4) ? 0 : 2;
 }
