@@ -234,7 +234,7 @@ struct bltc_ctx {
   DBuf<double> rows;
   int64_t n_moments = 0;
   DBuf<double> s_nodes, w_nodes;
-  DBuf<double> out_sorted, far_out, phi_dev;
+  DBuf<double> out_sorted, far_out, carry, phi_dev;
   DBuf<double4> src4;
   DBuf<int32_t> item_cnt, item_off, counters;
   DBuf<int2> items, items2;
@@ -514,7 +514,10 @@ void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, 
   a.yk = make_yukawa_k(p->kappa);
   c->out_sorted.resize(T.n);
   a.out = c->out_sorted.p;
-  const bool parity_packed = p->mode == BLTC_MODE_PARITY && G == 1 &&
+  a.g_lo = 0;
+  a.g_hi = G;
+  a.par_first = a.par_last = 1;
+  const bool parity_packed = p->mode == BLTC_MODE_PARITY &&
                              packed_supported(p->kernel_code, p->degree) &&
                              !(std::getenv("BLTC_PARITY_PACKED") &&
                                std::atoi(std::getenv("BLTC_PARITY_PACKED")) == 0);
@@ -528,8 +531,21 @@ void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, 
     build_packed_items(a, c->pk_pc, c->pk_poff, c->pk_wcnt, c->pk_woff, c->pk_items,
                        c->pk_dmask, c->lists.n_direct, c->bs.scan_tmp, c->hs, st, &pi);
     float far_ms = 0, near_ms = 0;
-    launch_eval_packed(a, p->kernel_code, pi, c->counters.p, st, &far_ms, &near_ms, c->timing,
-                       true);
+    if (G > 1) {
+      c->carry.resize(T.n);
+      a.carry = c->carry.p;
+    }
+    // one far + near pass per source group, in owner order (decomp.py:437-454)
+    for (int g = 0; g < G; ++g) {
+      a.g_lo = g;
+      a.g_hi = g + 1;
+      a.par_first = g == 0;
+      a.par_last = g == G - 1;
+      float f = 0, n = 0;
+      launch_eval_packed(a, p->kernel_code, pi, c->counters.p, st, &f, &n, c->timing, true);
+      far_ms += f;
+      near_ms += n;
+    }
     if (stats) {
       stats->far_s = far_ms * 1e-3;
       stats->near_s = near_ms * 1e-3;
@@ -831,7 +847,7 @@ int bltc_destroy(bltc_ctx* c) {
     L.a_cnt.release(); L.d_cnt.release(); L.pairs.release();
     c->used.release(); c->mflag.release(); c->mpos.release(); c->mlist.release();
     c->rows.release(); c->s_nodes.release(); c->w_nodes.release(); c->out_sorted.release();
-    c->far_out.release(); c->phi_dev.release(); c->src4.release(); c->flag.release();
+    c->far_out.release(); c->carry.release(); c->phi_dev.release(); c->src4.release(); c->flag.release();
     c->widen.release(); c->item_cnt.release(); c->item_off.release(); c->counters.release();
     c->items.release(); c->items2.release();
     c->pk_pc.release(); c->pk_poff.release(); c->pk_wcnt.release(); c->pk_woff.release();

@@ -321,6 +321,10 @@ __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it
   const double ty[2] = {a.ty[L.i0], a.ty[L.i1]};
   const double tz[2] = {a.tz[L.i0], a.tz[L.i1]};
   double acc[2] = {0.0, 0.0};
+  if (PAR && !a.par_first) {   // later source group: continue the running out
+    acc[0] = a.far_out[L.i0];
+    acc[1] = a.far_out[L.i1];
+  }
 
   // segment list ranges (warp-uniform) into the header
   int maxlen = 0, mylen = 0;
@@ -329,8 +333,8 @@ __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it
     int e0 = 0, len = 0;
     if (lane < it.w) {
       const int64_t b = it.z + lane;
-      e0 = a.a_ptr[b * a.G];
-      len = a.a_ptr[(b + 1) * a.G] - e0;
+      e0 = a.a_ptr[b * a.G + a.g_lo];
+      len = a.a_ptr[b * a.G + a.g_hi] - e0;
     }
     H->e0[lane] = e0;
     H->len[lane] = len;
@@ -668,8 +672,8 @@ __device__ __forceinline__ bool near_stage(const EvalArgs& a, const uint8_t* dma
 
 // PAR: the direct sums continue the far-field value of each target with
 // per-pair Neumaier compensation, out = acc + carry at the end (engine.py:
-// 302-312, 335) -- valid for one source group (the distributed forest's
-// per-owner interleaving goes through k_eval_parity).
+// 302-312, 335); over several source groups one pass per group, (acc, carry)
+// handed from pass to pass (decomp.py:437-454).
 template <int KIND, int CH, int FORM, bool PAR = false>
 __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 it,
                                                  const int32_t* poff, const uint8_t* dmask,
@@ -682,6 +686,10 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
   if (PAR) {
     acc[0] = a.far_out[L.i0];
     acc[1] = a.far_out[L.i1];
+    if (!a.par_first) {
+      comp[0] = a.carry[L.i0];
+      comp[1] = a.carry[L.i1];
+    }
   }
 
   Stream S[kGMax];
@@ -690,8 +698,8 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
     int e0 = 0, len = 0;
     if (k < it.w) {
       const int64_t b = it.z + k;
-      e0 = a.d_ptr[b * a.G];
-      len = a.d_ptr[(b + 1) * a.G] - e0;
+      e0 = a.d_ptr[b * a.G + a.g_lo];
+      len = a.d_ptr[b * a.G + a.g_hi] - e0;
     }
     stream_init(a, dmask, S[k], e0, len);
   }
@@ -757,6 +765,17 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
   // approximations first, then the compensated direct sums on top
   // (engine.py:302-312, 335)
   if (PAR) {
+    if (!a.par_last) {   // more source groups follow: keep (out, carry) apart
+      if (L.v0) {
+        a.far_out[L.i0] = acc[0];
+        a.carry[L.i0] = comp[0];
+      }
+      if (L.v1) {
+        a.far_out[L.i1] = acc[1];
+        a.carry[L.i1] = comp[1];
+      }
+      return;
+    }
     if (L.v0) a.out[L.i0] = __dadd_rn(acc[0], comp[0]);
     if (L.v1) a.out[L.i1] = __dadd_rn(acc[1], comp[1]);
     return;
