@@ -9,7 +9,7 @@ timeout 1200 python -m pytest tests -x -q -m gpu > gpurun_out/gpu_tests.log 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 900 python bench.py > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
 timeout 600 python bench.py --impl reference --steps 2 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-for c in c1 c2 c3; do
+for c in c1 c2 c3 c5; do
   timeout 600 python bench.py --config $c --steps 3 --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
 done
 # N > 1 flow on one GPU (test hook, not a reported number)
