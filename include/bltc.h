@@ -114,6 +114,16 @@ BLTC_API int bltc_treecode_device(bltc_ctx* ctx, const bltc_params* p, const dou
                          const double* q, int32_t coincident, double* phi_out,
                          bltc_stats* stats);
 
+/* Setup + precompute only: build_source_tree, build_target_batches,
+ * build_interaction_lists and the moments (compute_all_moments with
+ * all_moments = 1) on HOST buffers, no evaluation -- the structures are then
+ * read with the bltc_export_* calls below (tree.py:191-253, engine.py:128-130,
+ * moments.py:147-150).  stats: pair counts, setup / precompute times. */
+BLTC_API int bltc_build(bltc_ctx* ctx, const bltc_params* p, const double* cheb_s, int64_t n_t,
+                        const double* tx, const double* ty, const double* tz, int64_t n_s,
+                        const double* sx, const double* sy, const double* sz, const double* q,
+                        int32_t coincident, bltc_stats* stats);
+
 /* ---- Stage introspection of the last run (bit-exact checks) ------------- */
 typedef struct {
   int64_t n_sources, n_targets;

@@ -66,6 +66,9 @@ SIGNATURES = {
     "bltc_create": (ctypes.c_int, [ctypes.c_int, _vp, ctypes.POINTER(_vp)]),
     "bltc_destroy": (ctypes.c_int, [_vp]),
     "bltc_set_timing": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "bltc_build": (ctypes.c_int, [_vp, ctypes.POINTER(Params), _f64p, ctypes.c_int64,
+                                  _f64p, _f64p, _f64p, ctypes.c_int64, _f64p, _f64p, _f64p,
+                                  _f64p, ctypes.c_int32, ctypes.POINTER(Stats)]),
     "bltc_treecode": (ctypes.c_int, [_vp, ctypes.POINTER(Params), _f64p, ctypes.c_int64,
                                      _f64p, _f64p, _f64p, ctypes.c_int64, _f64p, _f64p, _f64p,
                                      _f64p, ctypes.c_int32, _f64p, ctypes.POINTER(Stats)]),

@@ -617,7 +617,8 @@ struct Trace {
 void run_pipeline(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64_t n_t,
                   const double* tx, const double* ty, const double* tz, int64_t n_s,
                   const double* sx, const double* sy, const double* sz, const double* q,
-                  bool coincident, double* phi_dev, bltc_stats* stats) {
+                  bool coincident, double* phi_dev, bltc_stats* stats,
+                  bool evaluate_phi = true) {
   check_params(p);
   if (n_s < 1 || n_t < 1) {
     set_error("cannot partition an empty particle set");
@@ -669,7 +670,8 @@ void run_pipeline(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64
   compute_moments(c, p, c->src, c->mac.p, c->ecl.p, p->all_moments ? 1 : 0, c->rows, 0);
   tr("moments");
   tm.mark();  // 2
-  // ---- compute: evaluation + un-permute
+  // ---- compute: evaluation + un-permute (skipped by bltc_build)
+  if (evaluate_phi) {
   {   // packed (x, y, z, q) records: FAST and the packed PARITY kernels
     c->src4.resize(n_s);
     k_pack4<<<grid_for(n_s, 256), 256, 0, st>>>(n_s, c->src.x.p, c->src.y.p, c->src.z.p,
@@ -681,6 +683,7 @@ void run_pipeline(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64
   k_unpermute<<<grid_for(n_t, 256), 256, 0, st>>>(n_t, c->out_sorted.p, c->tgt->perm.p, phi_dev);
   BLTC_LAUNCH_CHECK();
   tr("evaluate");
+  }
   tm.mark();  // 3
   if (stats) {
     unsigned long long* h = (unsigned long long*)c->hs.get(64);
@@ -878,6 +881,44 @@ int bltc_treecode_device(bltc_ctx* c, const bltc_params* p, const double* cheb_s
     if (stats) std::memset(stats, 0, sizeof(*stats));
     run_pipeline(c, p, cheb_s, n_t, tx, ty, tz, n_s, sx, sy, sz, q, coincident != 0, phi_out,
                  stats);
+  });
+}
+
+int bltc_build(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64_t n_t,
+               const double* tx, const double* ty, const double* tz, int64_t n_s,
+               const double* sx, const double* sy, const double* sz, const double* q,
+               int32_t coincident, bltc_stats* stats) {
+  return guarded([&] {
+    if (!c) throw UserError{BLTC_ERR_VALUE};
+    BLTC_CUDA(cudaSetDevice(c->device));
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    check_params(p);
+    if (n_s < 1 || n_t < 1) {
+      set_error("cannot partition an empty particle set");
+      throw UserError{BLTC_ERR_VALUE};
+    }
+    require_ptr(sx, "sx");
+    require_ptr(sy, "sy");
+    require_ptr(sz, "sz");
+    require_ptr(q, "q");
+    if (!coincident) {
+      require_ptr(tx, "tx");
+      require_ptr(ty, "ty");
+      require_ptr(tz, "tz");
+    }
+    cudaStream_t st = c->st;
+    const double* hs_[7] = {tx, ty, tz, sx, sy, sz, q};
+    const int64_t ns_[7] = {n_t, n_t, n_t, n_s, n_s, n_s, n_s};
+    for (int k = 0; k < 7; ++k) {
+      if (coincident && k < 3) continue;
+      c->in[k].resize(ns_[k]);
+      BLTC_CUDA(cudaMemcpyAsync(c->in[k].p, hs_[k], ns_[k] * sizeof(double),
+                                cudaMemcpyHostToDevice, st));
+    }
+    const bool co = coincident != 0;
+    run_pipeline(c, p, cheb_s, n_t, co ? c->in[3].p : c->in[0].p, co ? c->in[4].p : c->in[1].p,
+                 co ? c->in[5].p : c->in[2].p, n_s, c->in[3].p, c->in[4].p, c->in[5].p,
+                 c->in[6].p, co, nullptr, stats, false);
   });
 }
 

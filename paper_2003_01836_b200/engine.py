@@ -164,6 +164,30 @@ class Context:
             1 if coincident else 0, _lib.f64p(phi), ctypes.byref(st)))
         return phi, RunStats.from_c(st)
 
+    def build(self, system, config, mode: str | None = None, all_moments: bool = True
+              ) -> RunStats:
+        """Tree, batches, lists and moments only (no evaluation): the setup and
+        precompute phases of treecode_potentials (engine.py:353-362); read the
+        structures with export_tree / export_batches / export_lists /
+        export_moments."""
+        p = make_params(config, mode, all_moments)
+        t, s = system.targets, system.sources
+        coincident = t is s
+        sx, sy, sz = _f64(s.x), _f64(s.y), _f64(s.z)
+        q = _f64(system.charges)
+        if q.shape[0] != sx.shape[0]:
+            raise ValueError("one charge per source particle required")
+        tx, ty, tz = (sx, sy, sz) if coincident else (_f64(t.x), _f64(t.y), _f64(t.z))
+        if sx.shape[0] == 0 or tx.shape[0] == 0:
+            raise ValueError("cannot partition an empty particle set")
+        st = _lib.Stats()
+        _lib.check(self._lib.bltc_build(
+            self.handle, ctypes.byref(p), _lib.f64p(cheb_nodes(p.degree)), tx.shape[0],
+            _lib.f64p(tx), _lib.f64p(ty), _lib.f64p(tz), sx.shape[0], _lib.f64p(sx),
+            _lib.f64p(sy), _lib.f64p(sz), _lib.f64p(q), 1 if coincident else 0,
+            ctypes.byref(st)))
+        return RunStats.from_c(st)
+
     def treecode_device(self, params: _lib.Params, n_t, tx, ty, tz, n_s, sx, sy, sz, q,
                         coincident: bool, phi_ptr) -> RunStats:
         """Device-pointer variant (inputs resident in HBM): raw integer pointers."""

@@ -93,6 +93,31 @@ def test_structures_and_moments_bit_exact(bltc, ctx, case):
     _phi_check(phi, g["phi"], int(g["kind"]), exact=True)
 
 
+@pytest.mark.parametrize("case", ["c1_coulomb", "plummer", "deg8"])
+def test_build_only_structures_bit_exact(bltc, case):
+    """bltc_build: setup + moments without an evaluation, same structures."""
+    g = golden(case)
+    c = bltc.Context(0)
+    st = c.build(golden_system(g), _config(bltc, g), mode="parity", all_moments=True)
+    t = c.export_tree(0)
+    np.testing.assert_array_equal(t["perm"], g["tree_perm"])
+    np.testing.assert_array_equal(t["start"], g["tree_start"])
+    np.testing.assert_array_equal(t["lo"], g["tree_lo"])
+    b = c.export_batches()
+    np.testing.assert_array_equal(b["start"], g["batch_start"])
+    np.testing.assert_array_equal(b["radius"], g["batch_radius"])
+    L = c.export_lists()
+    np.testing.assert_array_equal(L["a_idx"], g["lists_approx_idx"])
+    np.testing.assert_array_equal(L["d_idx"], g["lists_direct_idx"])
+    ids, rows = c.export_moments()
+    elig = np.nonzero(g["moments_has"])[0]
+    np.testing.assert_array_equal(ids, elig)
+    np.testing.assert_array_equal(rows, g["moments"][elig])
+    assert (st.direct_pairs, st.approx_pairs) == (int(g["direct_pairs"]), int(g["approx_pairs"]))
+    assert st.compute_s == 0.0 or st.compute_s < 1e-3
+    c.close()
+
+
 @pytest.mark.parametrize("case", CASES)
 def test_parity_mode_potentials(bltc, case):
     g = golden(case)
