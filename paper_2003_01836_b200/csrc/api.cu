@@ -240,6 +240,7 @@ struct bltc_ctx {
   DBuf<int2> items, items2;
   DBuf<int32_t> pk_pc, pk_poff, pk_wcnt, pk_woff;   // packed FAST items
   DBuf<int4> pk_items;
+  PackedOrder pk_order;                              // cost-ordered copies
   DBuf<int32_t> need;   // LET step one flags (bltc_rank_needs)
   DBuf<uint8_t> pk_dmask;
   DBuf<double> partial;
@@ -528,7 +529,7 @@ void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, 
     a.far_out = c->far_out.p;
     c->counters.resize(2);
     PackedItems pi;
-    build_packed_items(a, c->pk_pc, c->pk_poff, c->pk_wcnt, c->pk_woff, c->pk_items,
+    build_packed_items(a, c->pk_order, c->pk_pc, c->pk_poff, c->pk_wcnt, c->pk_woff, c->pk_items,
                        c->pk_dmask, c->lists.n_direct, c->bs.scan_tmp, c->hs, st, &pi);
     float far_ms = 0, near_ms = 0;
     if (G > 1) {
@@ -560,7 +561,7 @@ void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, 
     c->counters.resize(2);
     if (packed_supported(p->kernel_code, p->degree)) {
       PackedItems pi;
-      build_packed_items(a, c->pk_pc, c->pk_poff, c->pk_wcnt, c->pk_woff, c->pk_items,
+      build_packed_items(a, c->pk_order, c->pk_pc, c->pk_poff, c->pk_wcnt, c->pk_woff, c->pk_items,
                          c->pk_dmask, c->lists.n_direct, c->bs.scan_tmp, c->hs, st, &pi);
       if (packed_preferred(p->kernel_code, pi.chunk_lane_eff)) {
         launch_eval_packed(a, p->kernel_code, pi, c->counters.p, st, &far_ms, &near_ms,
@@ -854,7 +855,9 @@ int bltc_destroy(bltc_ctx* c) {
     c->widen.release(); c->item_cnt.release(); c->item_off.release(); c->counters.release();
     c->items.release(); c->items2.release();
     c->pk_pc.release(); c->pk_poff.release(); c->pk_wcnt.release(); c->pk_woff.release();
-    c->pk_items.release(); c->pk_dmask.release(); c->need.release(); c->partial.release(); c->dpartial.release();
+    c->pk_items.release(); c->pk_dmask.release();
+    c->pk_order.far.release(); c->pk_order.near.release(); c->pk_order.cost.release();
+    c->pk_order.cost_sorted.release(); c->pk_order.tmp.release(); c->need.release(); c->partial.release(); c->dpartial.release();
     c->didx.release(); c->dout.release(); c->f_ecl.release(); c->f_mac.release(); c->f_x.release();
     c->f_y.release(); c->f_z.release(); c->f_q.release(); c->f_rows.release();
     c->f_src4.release();

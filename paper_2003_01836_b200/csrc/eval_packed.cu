@@ -30,6 +30,8 @@
 // (one source group; the distributed forest uses eval_parity.cu).
 // Measured choices: kGMax = 4, two targets per lane, 8 warps x
 // 2 CTAs per SM (register bound), k2 unrolled by 3, dy^2 in shared memory.
+#include <cub/device/device_radix_sort.cuh>
+
 #include "bltc_internal.cuh"
 #include "eval_common.cuh"
 
@@ -838,7 +840,7 @@ void far_packed_launch(const EvalArgs& a, const PackedItems& it, int* counter, c
   auto kern = k_far_packed<KIND, M, MINB, KU, FORM, PAR, DY>;
   BLTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = persistent_grid(kern, kWarps * 32, smem);
-  kern<<<grid, kWarps * 32, smem, st>>>(a, it.items, it.n_items, it.poff, counter);
+  kern<<<grid, kWarps * 32, smem, st>>>(a, it.items_far, it.n_items, it.poff, counter);
   BLTC_LAUNCH_CHECK();
 }
 
@@ -882,7 +884,8 @@ void near_packed_launch(const EvalArgs& a, const PackedItems& it, int* counter,
   auto kern = k_near_packed<KIND, CH, 2, FORM, PAR>;
   BLTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = persistent_grid(kern, kWarps * 32, smem);
-  kern<<<grid, kWarps * 32, smem, st>>>(a, it.items, it.n_items, it.poff, it.dmask, counter);
+  kern<<<grid, kWarps * 32, smem, st>>>(a, it.items_near, it.n_items, it.poff, it.dmask,
+                                        counter);
   BLTC_LAUNCH_CHECK();
 }
 }  // namespace
@@ -902,7 +905,39 @@ bool packed_supported(int kind, int degree) {
   return m == 5 || m == 6 || m == 8 || m == 9 || m == 11;
 }
 
-void build_packed_items(const EvalArgs& a, DBuf<int32_t>& pc, DBuf<int32_t>& poff,
+namespace {
+// Per item the number of lockstep steps of each kernel: far = the longest
+// approximation list among its segments, near = the most direct-list
+// sources among its segments (chunks of kNearCh per step).
+__global__ void k_item_costs(int n_items, const int4* __restrict__ items, EvalArgs a,
+                             uint32_t* __restrict__ cost_far, uint32_t* __restrict__ cost_near) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_items) return;
+  const int4 it = items[i];
+  uint32_t mf = 0, mn = 0;
+  for (int k = 0; k < it.w; ++k) {
+    const int64_t b = it.z + k;
+    const int32_t la = a.a_ptr[(b + 1) * a.G] - a.a_ptr[b * a.G];
+    uint32_t ns = 0;
+    for (int e = a.d_ptr[b * a.G]; e < a.d_ptr[(b + 1) * a.G]; ++e) {
+      const EvalCluster& c = a.clusters[a.d_idx[e]];
+      ns += (uint32_t)(c.stop - c.start);
+    }
+    mf = max(mf, (uint32_t)la);
+    mn = max(mn, ns);
+  }
+  cost_far[i] = mf;
+  cost_near[i] = mn;
+}
+
+bool tune_item_sort() {
+  const char* e = std::getenv("BLTC_ITEM_SORT");
+  return e ? std::atoi(e) != 0 : true;
+}
+}  // namespace
+
+void build_packed_items(const EvalArgs& a, PackedOrder& order, DBuf<int32_t>& pc,
+                        DBuf<int32_t>& poff,
                         DBuf<int32_t>& wcnt, DBuf<int32_t>& woff, DBuf<int4>& items,
                         DBuf<uint8_t>& dmask, int64_t n_direct, DBuf<int32_t>& scan_tmp,
                         HostScratch& hs, cudaStream_t st, PackedItems* out) {
@@ -954,8 +989,34 @@ void build_packed_items(const EvalArgs& a, DBuf<int32_t>& pc, DBuf<int32_t>& pof
     }
   }
   out->items = items.p;
+  out->items_far = items.p;
+  out->items_near = items.p;
   out->poff = poff.p;
   out->dmask = dmask.p;
+  const int n = out->n_items;
+  if (n > 1 && tune_item_sort()) {
+    // longest-processing-time-first order for the persistent kernels' atomic
+    // work counter (item order does not change any result)
+    order.far.resize(n);
+    order.near.resize(n);
+    order.cost.resize(2 * (size_t)n);
+    order.cost_sorted.resize(n);
+    k_item_costs<<<(n + 255) / 256, 256, 0, st>>>(n, items.p, a, order.cost.p,
+                                                  order.cost.p + n);
+    BLTC_LAUNCH_CHECK();
+    size_t bytes = 0;
+    BLTC_CUDA(cub::DeviceRadixSort::SortPairsDescending(
+        nullptr, bytes, order.cost.p, order.cost_sorted.p, items.p, order.far.p, n, 0, 32, st));
+    order.tmp.resize(bytes + 1);
+    BLTC_CUDA(cub::DeviceRadixSort::SortPairsDescending(order.tmp.p, bytes, order.cost.p,
+                                                        order.cost_sorted.p, items.p,
+                                                        order.far.p, n, 0, 32, st));
+    BLTC_CUDA(cub::DeviceRadixSort::SortPairsDescending(order.tmp.p, bytes, order.cost.p + n,
+                                                        order.cost_sorted.p, items.p,
+                                                        order.near.p, n, 0, 32, st));
+    out->items_far = order.far.p;
+    out->items_near = order.near.p;
+  }
 }
 
 void launch_eval_packed(const EvalArgs& a, int kind, const PackedItems& it, int* counters,
