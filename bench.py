@@ -39,13 +39,15 @@ CONFIGS = {
     # BASELINE.json configs; c4 is the metric's workload (8M Coulomb n=8 theta=0.8)
     "c1": dict(workload="C1: N=20k uniform cube, Coulomb, n=4, theta=0.7", gen="uniform",
                n=20_000, kind=0, kappa=0.0, degree=4, theta=0.7, leaf=2000, batch=2000),
-    # C2/C3: N_B=1000 (= 500 for this uniform cube) measured fastest on B200:
-    # C2 53 ms vs 75 ms at N_B=2000, C3 163 ms vs 221 ms (tools/sweep_c4.py)
+    # C2/C3: N_B=160 (= any of 64..200 for this uniform cube: octree level-5
+    # batches of ~30 targets) measured fastest on B200 with packed, longest-
+    # first items: C2 42 ms vs 50 ms at N_B=1000 and 47 ms at 250, C3 101 ms
+    # vs 121 / 115 ms (tools/sweep_c4.py)
     "c2": dict(workload="C2: N=1M uniform cube, Coulomb, n=8, theta=0.8", gen="uniform",
-               n=1_000_000, kind=0, kappa=0.0, degree=8, theta=0.8, leaf=2000, batch=1000),
+               n=1_000_000, kind=0, kappa=0.0, degree=8, theta=0.8, leaf=2000, batch=160),
     "c3": dict(workload="C3: N=1M uniform cube, Yukawa kappa=0.5, n=8, theta=0.8",
                gen="uniform", n=1_000_000, kind=1, kappa=0.5, degree=8, theta=0.8, leaf=2000,
-               batch=1000),
+               batch=160),
     # N_B (batch size) is the performance knob; the CPU
     # baseline / reference arm run with the same value.  160 is the fastest
     # measured for C4 on B200 with packed work items (N_B=125: 0.929 s,
@@ -56,8 +58,9 @@ CONFIGS = {
                batch=160),
     "c4u": dict(workload="N=8M uniform cube, Coulomb, n=8, theta=0.8", gen="uniform",
                 n=8_000_000, kind=0, kappa=0.0, degree=8, theta=0.8, leaf=2000, batch=2000),
+    # C5: N_B=160 (level-7 batches): 10.1 s vs 11.2 s at 250 and 11.7 s at 1000
     "c5": dict(workload="C5: N=64M uniform cube, Coulomb, n=10, theta=0.7", gen="uniform",
-               n=64_000_000, kind=0, kappa=0.0, degree=10, theta=0.7, leaf=2000, batch=1000),
+               n=64_000_000, kind=0, kappa=0.0, degree=10, theta=0.7, leaf=2000, batch=160),
     # the paper's strong-scaling case (16.2 s on 32 P100)
     "paper64m": dict(workload="64M uniform cube, Coulomb, n=8, theta=0.8, N_L=N_B=4000 "
                               "(paper strong-scaling case)", gen="uniform", n=64_000_000,

@@ -891,10 +891,13 @@ void near_packed_launch(const EvalArgs& a, const PackedItems& it, int* counter,
 }  // namespace
 
 bool packed_preferred(int kind, double chunk_lane_eff) {
-  if (const char* e = std::getenv("BLTC_PACK"))
-    if (std::atoi(e) == 1) return true;   // forced on
+  // With longest-first item order the packed kernels are at least as fast as
+  // the per-batch ones at every measured batch size, including full batches
+  // (N_B = 2000: C2 71.9 vs 73.3 ms, C3 169.9 vs 175.4, C4 1146 vs 1163);
+  // BLTC_PACK=0 (packed_supported) still selects the per-batch kernels.
   (void)kind;
-  return chunk_lane_eff < 0.95;
+  (void)chunk_lane_eff;
+  return true;
 }
 
 bool packed_supported(int kind, int degree) {
