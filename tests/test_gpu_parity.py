@@ -222,6 +222,7 @@ def test_deterministic_repeats(bltc):
     ("uniform", 200_000, 2000, 2000, 8, 0.8),
     ("plummer", 200_000, 2000, 1000, 8, 0.8),
     ("uniform", 150_000, 1000, 500, 10, 0.7),
+    ("uniform", 150_000, 2000, 160, 8, 0.8),    # the C2/C3 bench batch size
 ])
 def test_oracle_parity_mid_size(bltc, ctx, oracle, gen, n, leaf, batch, deg, theta):
     """Mid-size runs against the oracle: structures bit-exact, PARITY phi
