@@ -128,6 +128,39 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// Bulk (TMA-engine) copies global -> shared with mbarrier completion
+// (cp.async.bulk, SASS UBLKCP): one instruction moves a whole contiguous run.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ int next_item(int* counter) {
   int it = 0;
   if ((threadIdx.x & 31) == 0) it = atomicAdd(counter, 1);
@@ -600,11 +633,11 @@ __device__ __forceinline__ void stream_init(const EvalArgs& a, const uint8_t* dm
   if (len > 1) stream_entry(a, dmask, e0 + 1, &S.ns, &S.nn, &S.nm);
 }
 
-// Stage record o + r of the stream into dst[r]; returns whether it may form
-// singular pairs.
-__device__ __forceinline__ bool stream_stage(const EvalArgs& a, const uint8_t* dmask,
-                                             const Stream& S, double4* dst, int r0) {
-  bool need_mask = false;
+// Source index of record o + r0 of the stream (-1: past its end); need_mask:
+// the record may form singular pairs.
+__device__ __forceinline__ int stream_src(const EvalArgs& a, const uint8_t* dmask,
+                                          const Stream& S, int r0, bool& need_mask) {
+  need_mask = false;
   int src = -1;
   if (S.e < S.len) {
     const int r = S.o + r0;
@@ -630,6 +663,15 @@ __device__ __forceinline__ bool stream_stage(const EvalArgs& a, const uint8_t* d
       }
     }
   }
+  return src;
+}
+
+// Stage record o + r of the stream into dst[r]; returns whether it may form
+// singular pairs.
+__device__ __forceinline__ bool stream_stage(const EvalArgs& a, const uint8_t* dmask,
+                                             const Stream& S, double4* dst, int r0) {
+  bool need_mask;
+  const int src = stream_src(a, dmask, S, r0, need_mask);
   if (src >= 0) {
     const double4* sp = a.src4 + src;
     cp_async16(dst + r0, sp);
@@ -672,14 +714,56 @@ __device__ __forceinline__ bool near_stage(const EvalArgs& a, const uint8_t* dma
   return __any_sync(0xffffffffu, need_mask);
 }
 
+// BULK: the same chunk staged by the TMA engine.  Each segment's 32 records
+// are runs of consecutive sources (a cluster's tail, the next cluster's
+// head, ...): the first lane of each run issues one cp.async.bulk of the
+// whole run; lane 0 first arms the buffer's mbarrier with the chunk's byte
+// count; past-the-end records are written as zero-charge padding.
+template <int CH>
+__device__ __forceinline__ bool near_stage_bulk(const EvalArgs& a, const uint8_t* dmask,
+                                                Stream (&S)[kGMax], double4* wsm, int buf,
+                                                int lane, uint64_t* bar) {
+  static_assert(CH == 32, "bulk staging: one record per lane");
+  bool need_mask = false;
+  int src[kGMax];
+  unsigned total = 0;
+#pragma unroll
+  for (int k = 0; k < kGMax; ++k) {
+    bool m;
+    src[k] = stream_src(a, dmask, S[k], lane, m);
+    need_mask |= m;
+    total += 32u * __popc(__ballot_sync(0xffffffffu, src[k] >= 0));
+    stream_advance<CH>(a, dmask, S[k]);
+  }
+  if (lane == 0) mbar_arrive_expect_tx(bar, total * 1u);
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < kGMax; ++k) {
+    double4* dst = wsm + k * NearSmem<CH>::kSeg + buf * CH;
+    const int prev = __shfl_up_sync(0xffffffffu, src[k], 1);
+    const bool valid = src[k] >= 0;
+    const bool lead = valid && (lane == 0 || prev != src[k] - 1);
+    const unsigned ends = __ballot_sync(0xffffffffu, lead || !valid);
+    if (lead) {
+      const unsigned later = lane == 31 ? 0u : ends >> (lane + 1);
+      const int len = later ? __ffs(later) : 32 - lane;
+      bulk_g2s(dst + lane, a.src4 + src[k], 32u * len, bar);
+    } else if (!valid) {
+      dst[lane] = make_double4(1e150, 1e150, 1e150, 0.0);   // contributes exactly 0
+    }
+  }
+  return __any_sync(0xffffffffu, need_mask);
+}
+
 // PAR: the direct sums continue the far-field value of each target with
 // per-pair Neumaier compensation, out = acc + carry at the end (engine.py:
 // 302-312, 335); over several source groups one pass per group, (acc, carry)
 // handed from pass to pass (decomp.py:437-454).
-template <int KIND, int CH, int FORM, bool PAR = false>
+template <int KIND, int CH, int FORM, bool PAR = false, bool BULK = false>
 __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 it,
                                                  const int32_t* poff, const uint8_t* dmask,
-                                                 double4* wsm, int lane) {
+                                                 double4* wsm, int lane, uint64_t* bar,
+                                                 unsigned& phase) {
   const LaneTargets L = lane_targets(it, a, poff, lane);
   const double tx[2] = {a.tx[L.i0], a.tx[L.i1]};
   const double ty[2] = {a.ty[L.i0], a.ty[L.i1]};
@@ -711,13 +795,18 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
   for (int k = 0; k < kGMax; ++k) live |= S[k].e < S[k].len;
   if (live) {
     __syncwarp();
-    bool masked = near_stage<CH>(a, dmask, S, wsm, 0, lane);
+    bool masked = BULK ? near_stage_bulk<CH>(a, dmask, S, wsm, 0, lane, bar)
+                       : near_stage<CH>(a, dmask, S, wsm, 0, lane);
     for (int buf = 0;; buf ^= 1) {
       bool more = false;
 #pragma unroll
       for (int k = 0; k < kGMax; ++k) more |= S[k].e < S[k].len;
       bool masked_next = false;
-      if (more) {
+      if constexpr (BULK) {
+        if (more) masked_next = near_stage_bulk<CH>(a, dmask, S, wsm, buf ^ 1, lane, bar + (buf ^ 1));
+        mbar_wait(bar + buf, (phase >> buf) & 1u);
+        phase ^= 1u << buf;
+      } else if (more) {
         masked_next = near_stage<CH>(a, dmask, S, wsm, buf ^ 1, lane);
         cp_async_wait<1>();
       } else {
@@ -794,16 +883,24 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
   }
 }
 
-template <int KIND, int CH, int MINB, int FORM, bool PAR = false>
+template <int KIND, int CH, int MINB, int FORM, bool PAR = false, bool BULK = false>
 __global__ void __launch_bounds__(kWarps * 32, MINB)
 k_near_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int32_t* poff,
               const uint8_t* dmask, int* counter) {
   extern __shared__ double4 nsmem[];
+  __shared__ uint64_t nbar[kWarps][2];   // BULK: one mbarrier per staging buffer
   double4* smem = nsmem;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double4* wsm = smem + warp * NearSmem<CH>::kWarp;
+  if (BULK && lane == 0) {
+    mbar_init(&nbar[warp][0], 1);
+    mbar_init(&nbar[warp][1], 1);
+  }
+  __syncwarp();
+  unsigned phase = 0;
   for (int item = next_item(counter); item < n_items; item = next_item(counter))
-    near_packed_item<KIND, CH, FORM, PAR>(a, items[item], poff, dmask, wsm, lane);
+    near_packed_item<KIND, CH, FORM, PAR, BULK>(a, items[item], poff, dmask, wsm, lane,
+                                                nbar[warp], phase);
 }
 
 // ---------------------------------------------------------------------------
@@ -812,6 +909,10 @@ int tune_far_unroll(int kind) {
   const char* e = std::getenv("BLTC_FAR_UNROLL");
   // Coulomb: 3 rows per step, -2% far time at C4 (measured)
   return e ? std::atoi(e) : (kind == 0 ? 3 : 1);
+}
+int tune_near_bulk() {
+  const char* e = std::getenv("BLTC_NEAR_BULK");
+  return e ? std::atoi(e) : 0;
 }
 int tune_far_dy() {
   const char* e = std::getenv("BLTC_FAR_DY");
@@ -881,7 +982,8 @@ template <int KIND, int CH = kNearCh, int FORM = 0, bool PAR = false>
 void near_packed_launch(const EvalArgs& a, const PackedItems& it, int* counter,
                         cudaStream_t st) {
   const size_t smem = sizeof(double4) * kWarps * NearSmem<CH>::kWarp;
-  auto kern = k_near_packed<KIND, CH, 2, FORM, PAR>;
+  auto kern = tune_near_bulk() ? k_near_packed<KIND, CH, 2, FORM, PAR, true>
+                               : k_near_packed<KIND, CH, 2, FORM, PAR, false>;
   BLTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = persistent_grid(kern, kWarps * 32, smem);
   kern<<<grid, kWarps * 32, smem, st>>>(a, it.items_near, it.n_items, it.poff, it.dmask,
