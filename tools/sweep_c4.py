@@ -20,6 +20,7 @@ ap.add_argument("--config", default="c4")
 ap.add_argument("--leaf", default="2000")
 ap.add_argument("--batch", default="500")
 ap.add_argument("--steps", type=int, default=2)
+ap.add_argument("--mode", default="fast", choices=["fast", "parity"])
 ap.add_argument("--env", default="", help="semicolon-separated KEY=VAL sets to try, '|'-joined")
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
@@ -39,7 +40,7 @@ for env in envsets:
     for leaf in map(int, args.leaf.split(",")):
         for batch in map(int, args.batch.split(",")):
             econf = bench.eval_config(cfg, batch, leaf)
-            params = engine.make_params(econf, "fast")
+            params = engine.make_params(econf, args.mode)
             def step():
                 return ctx.treecode_device(params, n, p[0], p[1], p[2], n, p[0], p[1], p[2],
                                            p[3], True, phi.data_ptr())
