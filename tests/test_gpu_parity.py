@@ -315,3 +315,20 @@ def test_packed_items_ragged_batches(bltc, batch, leaf, deg):
         _phi_check(phi, ref, 0, exact=False)
         if force and deg + 1 in (5, 6, 8, 9, 11):
             assert st.packed == 1
+
+
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+def test_schedule_variants_bitwise_equal(bltc, mode, monkeypatch):
+    """Work-item order (longest-first vs stream order) and the near-field
+    staging engine (cp.async vs cp.async.bulk) change no bit of the result."""
+    from paper_2003_01836_b200 import cli
+    s = cli.generate_plummer(60_000, 13)
+    cfg = bltc.EvalConfig(theta=0.8, degree=8, leaf_size=1000, batch_size=160)
+    base, _ = bltc.treecode_potentials(s, cfg, mode=mode)
+    for env in ({"BLTC_ITEM_SORT": "0"}, {"BLTC_NEAR_BULK": "1"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        phi, _ = bltc.treecode_potentials(s, cfg, mode=mode)
+        for k in env:
+            monkeypatch.delenv(k)
+        np.testing.assert_array_equal(phi, base)
