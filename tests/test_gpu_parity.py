@@ -332,3 +332,17 @@ def test_schedule_variants_bitwise_equal(bltc, mode, monkeypatch):
         for k in env:
             monkeypatch.delenv(k)
         np.testing.assert_array_equal(phi, base)
+
+
+@pytest.mark.parametrize("kappa", [1e-3, 5.0, 400.0, 5000.0])
+def test_fast_yukawa_kappa_range(bltc, kappa):
+    """FAST's folded-kappa exp (clamped at kappa r = 700) against PARITY over
+    screening lengths from nearly Coulomb to underflowing far fields."""
+    from paper_2003_01836_b200 import cli
+    s = cli.generate_particles(40_000, 5)
+    cfg = bltc.EvalConfig(theta=0.7, degree=8, leaf_size=500, batch_size=160,
+                          kernel=bltc.yukawa(kappa))
+    ref, _ = bltc.treecode_potentials(s, cfg, mode="parity")
+    phi, _ = bltc.treecode_potentials(s, cfg, mode="fast")
+    assert np.all(np.isfinite(phi))
+    assert np.abs(phi - ref).max() <= 1e-13 * np.abs(ref).max()
