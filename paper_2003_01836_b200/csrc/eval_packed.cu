@@ -949,11 +949,12 @@ template <int KIND>
 bool far_packed_dispatch_parity(const EvalArgs& a, const PackedItems& it, int* counter,
                                 cudaStream_t st) {
   switch (a.degree + 1) {
-    case 5: far_packed_launch<KIND, 5, 1, 0, 2, true>(a, it, counter, st); return true;
-    case 6: far_packed_launch<KIND, 6, 1, 0, 2, true>(a, it, counter, st); return true;
-    case 8: far_packed_launch<KIND, 8, 1, 0, 2, true>(a, it, counter, st); return true;
-    case 9: far_packed_launch<KIND, 9, 1, 0, 2, true>(a, it, counter, st); return true;
-    case 11: far_packed_launch<KIND, 11, 1, 0, 2, true>(a, it, counter, st); return true;
+#define BLTC_PAR_CASE(MM) \
+    case MM: far_packed_launch<KIND, MM, 1, 0, 2, true>(a, it, counter, st); return true;
+    BLTC_PAR_CASE(2) BLTC_PAR_CASE(3) BLTC_PAR_CASE(4) BLTC_PAR_CASE(5) BLTC_PAR_CASE(6)
+    BLTC_PAR_CASE(7) BLTC_PAR_CASE(8) BLTC_PAR_CASE(9) BLTC_PAR_CASE(10) BLTC_PAR_CASE(11)
+    BLTC_PAR_CASE(12) BLTC_PAR_CASE(13)
+#undef BLTC_PAR_CASE
     default: return false;
   }
 }
@@ -962,9 +963,12 @@ template <int KIND>
 bool far_packed_dispatch(const EvalArgs& a, const PackedItems& it, int* counter,
                          cudaStream_t st) {
   switch (a.degree + 1) {
-    case 5: far_packed_launch<KIND, 5>(a, it, counter, st); return true;
-    case 6: far_packed_launch<KIND, 6>(a, it, counter, st); return true;
-    case 8: far_packed_launch<KIND, 8>(a, it, counter, st); return true;
+#define BLTC_FAST_CASE(MM) \
+    case MM: far_packed_launch<KIND, MM>(a, it, counter, st); return true;
+    BLTC_FAST_CASE(2) BLTC_FAST_CASE(3) BLTC_FAST_CASE(4) BLTC_FAST_CASE(5) BLTC_FAST_CASE(6)
+    BLTC_FAST_CASE(7) BLTC_FAST_CASE(8) BLTC_FAST_CASE(10) BLTC_FAST_CASE(11)
+    BLTC_FAST_CASE(12) BLTC_FAST_CASE(13)
+#undef BLTC_FAST_CASE
     case 9:
       // tuned for the benchmark degree: k2 unrolled by 3, FORM 2 (measured)
       if (tune_form() != 2) far_packed_launch<KIND, 9, 1, 0>(a, it, counter, st);
@@ -973,7 +977,6 @@ bool far_packed_dispatch(const EvalArgs& a, const PackedItems& it, int* counter,
       else if (tune_far_unroll(KIND) == 3) far_packed_launch<KIND, 9, 3, 2>(a, it, counter, st);
       else far_packed_launch<KIND, 9, 1, 2>(a, it, counter, st);
       return true;
-    case 11: far_packed_launch<KIND, 11>(a, it, counter, st); return true;
     default: return false;
   }
 }
@@ -1007,7 +1010,7 @@ bool packed_supported(int kind, int degree) {
     if (std::atoi(e) == 0) return false;
   if (kind != 0 && kind != 1) return false;
   const int m = degree + 1;
-  return m == 5 || m == 6 || m == 8 || m == 9 || m == 11;
+  return m >= 2 && m <= 13;   // degrees 1..12 (the paper's sweeps); others per-batch
 }
 
 namespace {

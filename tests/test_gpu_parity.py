@@ -313,7 +313,7 @@ def test_packed_items_ragged_batches(bltc, batch, leaf, deg):
         finally:
             os.environ.pop("BLTC_PACK", None)
         _phi_check(phi, ref, 0, exact=False)
-        if force and deg + 1 in (5, 6, 8, 9, 11):
+        if force:
             assert st.packed == 1
 
 
@@ -346,3 +346,27 @@ def test_fast_yukawa_kappa_range(bltc, kappa):
     phi, _ = bltc.treecode_potentials(s, cfg, mode="fast")
     assert np.all(np.isfinite(phi))
     assert np.abs(phi - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("deg", list(range(1, 13)))
+def test_every_packed_degree(bltc, oracle, deg, monkeypatch):
+    """Degrees 1..12 run on the packed kernels: PARITY bitwise the oracle and
+    the generic k_eval_parity path, FAST within tolerance of PARITY."""
+    import os
+    from paper_2003_01836_b200 import cli
+    s = cli.generate_particles(8000, 29)
+    src = s.sources
+    cfg = bltc.EvalConfig(theta=0.75, degree=deg, leaf_size=400, batch_size=100)
+    ref, _ = oracle.treecode_potentials(src.x, src.y, src.z, src.x, src.y, src.z, s.charges,
+                                        True, 0.75, deg, 400, 100, 0, 0.0,
+                                        threads=os.cpu_count() or 1)
+    phi_p, st = bltc.treecode_potentials(s, cfg, mode="parity")
+    np.testing.assert_array_equal(phi_p, ref)
+    assert st.packed == 1
+    monkeypatch.setenv("BLTC_PARITY_PACKED", "0")
+    phi_g, _ = bltc.treecode_potentials(s, cfg, mode="parity")
+    monkeypatch.delenv("BLTC_PARITY_PACKED")
+    np.testing.assert_array_equal(phi_g, ref)
+    phi_f, stf = bltc.treecode_potentials(s, cfg, mode="fast")
+    assert stf.packed == 1
+    _phi_check(phi_f, ref, 0, exact=False)
