@@ -24,6 +24,11 @@ __global__ void k_moments(const double* sx, const double* sy, const double* sz,
                           const int32_t* cstop, const double* lo, const double* hi,
                           const double* s_nodes, const double* w_nodes, int degree,
                           int mstride, double* rows);
+bool launch_moments_k1(const double* sx, const double* sy, const double* sz, const double* sq,
+                       const int32_t* list, int64_t n_list, const int32_t* cstart,
+                       const int32_t* cstop, const double* lo, const double* hi,
+                       const double* s_nodes, const double* w_nodes, int degree, int mstride,
+                       double* rows, cudaStream_t st);
 __global__ void k_lists(int64_t nb, int G, int g, const double* bcenter, const double* bradius,
                         const int32_t* bstart, const int32_t* bstop, const MacNode* nodes,
                         int32_t cluster_offset, double theta, int64_t per_node, bool fill,
@@ -460,10 +465,17 @@ void compute_moments(bltc_ctx* c, const bltc_params* p, const Partition& T, cons
     } else {
       int threads = ((m * m + 31) / 32) * 32;
       if (threads < 96) threads = 96;
-      k_moments<<<(unsigned)c->n_moments, threads, 0, st>>>(
-          T.x.p, T.y.p, T.z.p, T.q.p, c->mlist.p, T.start.p, T.stop.p, T.lo.p, T.hi.p,
-          c->s_nodes.p, c->w_nodes.p, p->degree, mstride, rows.p);
-      BLTC_LAUNCH_CHECK();
+      const char* old_env = std::getenv("BLTC_PARITY_MOMENTS_OLD");
+      const bool k1 = !(old_env && std::atoi(old_env) != 0) &&
+                      launch_moments_k1(T.x.p, T.y.p, T.z.p, T.q.p, c->mlist.p, c->n_moments,
+                                        T.start.p, T.stop.p, T.lo.p, T.hi.p, c->s_nodes.p,
+                                        c->w_nodes.p, p->degree, mstride, rows.p, st);
+      if (!k1) {
+        k_moments<<<(unsigned)c->n_moments, threads, 0, st>>>(
+            T.x.p, T.y.p, T.z.p, T.q.p, c->mlist.p, T.start.p, T.stop.p, T.lo.p, T.hi.p,
+            c->s_nodes.p, c->w_nodes.p, p->degree, mstride, rows.p);
+        BLTC_LAUNCH_CHECK();
+      }
     }
   }
 }
@@ -1482,10 +1494,13 @@ int bltc_stage_moments(bltc_ctx* c, const bltc_params* p, const double* cheb_s, 
     } else {
       int threads = ((m * m + 31) / 32) * 32;
       if (threads < 96) threads = 96;
-      k_moments<<<(unsigned)n_list, threads, 0, st>>>(S.x.p, S.y.p, S.z.p, S.q.p, c->mlist.p,
-                                                      S.start.p, S.stop.p, S.lo.p, S.hi.p,
-                                                      c->s_nodes.p, c->w_nodes.p, p->degree,
-                                                      mstride, c->rows.p);
+      if (!launch_moments_k1(S.x.p, S.y.p, S.z.p, S.q.p, c->mlist.p, n_list, S.start.p,
+                             S.stop.p, S.lo.p, S.hi.p, c->s_nodes.p, c->w_nodes.p, p->degree,
+                             mstride, c->rows.p, st))
+        k_moments<<<(unsigned)n_list, threads, 0, st>>>(S.x.p, S.y.p, S.z.p, S.q.p, c->mlist.p,
+                                                        S.start.p, S.stop.p, S.lo.p, S.hi.p,
+                                                        c->s_nodes.p, c->w_nodes.p, p->degree,
+                                                        mstride, c->rows.p);
       BLTC_LAUNCH_CHECK();
     }
     BLTC_CUDA(cudaMemcpy2DAsync(rows_out, m3 * sizeof(double), c->rows.p,
