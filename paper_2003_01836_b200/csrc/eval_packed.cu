@@ -1016,7 +1016,7 @@ bool packed_supported(int kind, int degree) {
 namespace {
 // Per item the number of lockstep steps of each kernel: far = the longest
 // approximation list among its segments, near = the most direct-list
-// sources among its segments (chunks of kNearCh per step).
+// sources among its segments (chunks of kNearCh per step), as a sort key.
 __global__ void k_item_costs(int n_items, const int4* __restrict__ items, EvalArgs a,
                              uint32_t* __restrict__ cost_far, uint32_t* __restrict__ cost_near) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1035,7 +1035,13 @@ __global__ void k_item_costs(int n_items, const int4* __restrict__ items, EvalAr
     mn = max(mn, ns);
   }
   cost_far[i] = mf;
-  cost_near[i] = mn;
+  // near: power-of-two cost classes, longest class first, stream order
+  // within a class -- concurrently running items then read neighbouring
+  // batches' (largely shared) direct-list sources while they sit in L2; an
+  // exact cost order scatters them (near DRAM reads 0.85 -> 76 GB per C4
+  // launch, at unchanged time)
+  const uint32_t cls = mn ? min(31u, 32u - (uint32_t)__clz(mn)) : 0u;
+  cost_near[i] = (cls << 27) | ((1u << 27) - 1u - (uint32_t)min(i, (1 << 27) - 1));
 }
 
 bool tune_item_sort() {
