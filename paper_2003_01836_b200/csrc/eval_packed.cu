@@ -978,7 +978,9 @@ bool far_packed_dispatch(const EvalArgs& a, const PackedItems& it, int* counter,
     case 9:
       // tuned for the benchmark degree: k2 unrolled by 3, FORM 2 (measured)
       if (tune_form() != 2) far_packed_launch<KIND, 9, 1, 0>(a, it, counter, st);
-      else if (KIND == 0 && tune_far_dy())
+      else if (KIND == 1)   // Yukawa: one CTA per SM, full register file (C3 far -4%)
+        far_packed_launch<KIND, 9, 3, 2, 1>(a, it, counter, st);
+      else if (tune_far_dy())
         far_packed_launch<KIND, 9, 3, 2, 2, false, true>(a, it, counter, st);
       else if (tune_far_unroll(KIND) == 3) far_packed_launch<KIND, 9, 3, 2>(a, it, counter, st);
       else far_packed_launch<KIND, 9, 1, 2>(a, it, counter, st);
