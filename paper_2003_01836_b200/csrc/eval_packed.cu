@@ -972,8 +972,14 @@ bool far_packed_dispatch(const EvalArgs& a, const PackedItems& it, int* counter,
 #define BLTC_FAST_CASE(MM) \
     case MM: far_packed_launch<KIND, MM>(a, it, counter, st); return true;
     BLTC_FAST_CASE(2) BLTC_FAST_CASE(3) BLTC_FAST_CASE(4) BLTC_FAST_CASE(5) BLTC_FAST_CASE(6)
-    BLTC_FAST_CASE(7) BLTC_FAST_CASE(8) BLTC_FAST_CASE(10) BLTC_FAST_CASE(11)
+    BLTC_FAST_CASE(7) BLTC_FAST_CASE(8) BLTC_FAST_CASE(10)
     BLTC_FAST_CASE(12) BLTC_FAST_CASE(13)
+    case 11:
+      // C5's degree: FORM 2 (C5 far 8382 -> 8282 ms; k2 x3 with one CTA per
+      // SM 8292, one CTA per SM alone 8700)
+      if (tune_form() == 2) far_packed_launch<KIND, 11, 1, 2>(a, it, counter, st);
+      else far_packed_launch<KIND, 11>(a, it, counter, st);
+      return true;
 #undef BLTC_FAST_CASE
     case 9:
       // tuned for the benchmark degree: k2 unrolled by 3, FORM 2 (measured)
