@@ -55,6 +55,26 @@ def test_run_distributed_requires_coincident():
         run_distributed(system, bltc.EvalConfig(theta=0.7, degree=3), ranks=2)
 
 
+def test_run_distributed_native_validates_before_the_device():
+    """The one-call C path raises the reference's ValueErrors (decomp.py:
+    85-88, 493-495) before touching a GPU."""
+    import paper_2003_01836_b200 as bltc
+    from paper_2003_01836_b200.decomp import run_distributed_native
+    rng = np.random.default_rng(98)
+    t = Points.from_array(rng.uniform(-1, 1, (50, 3)))
+    s = Points.from_array(rng.uniform(-1, 1, (50, 3)))
+    cfg = bltc.EvalConfig(theta=0.7, degree=3)
+    with pytest.raises(ValueError):
+        run_distributed_native(bltc.ParticleSystem(targets=t, sources=s,
+                                                   charges=rng.uniform(-1, 1, 50)), cfg, 2,
+                               devices=[0])
+    same = bltc.ParticleSystem.from_single_set(s, rng.uniform(-1, 1, 50))
+    with pytest.raises(ValueError):
+        run_distributed_native(same, cfg, 0, devices=[0])
+    with pytest.raises(ValueError):
+        run_distributed_native(same, cfg, 51, devices=[0])   # fewer particles than ranks
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
