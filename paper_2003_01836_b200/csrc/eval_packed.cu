@@ -955,7 +955,7 @@ bool far_packed_dispatch_parity(const EvalArgs& a, const PackedItems& it, int* c
       // the benchmark degree: one CTA per SM with the full register file and
       // k2 unrolled by 3 -- the IEEE sqrt / division chains want ILP more
       // than warps (C4 far 2151 -> 2054 ms; 2 CTAs per SM spill at 128 regs)
-      far_packed_launch<KIND, 9, 3, 0, 1, true>(a, it, counter, st);
+      far_packed_launch<KIND, 9, 3, 0, 1, true>(a, it, counter, st);   // x9: 2482 ms
       return true;
     BLTC_PAR_CASE(2) BLTC_PAR_CASE(3) BLTC_PAR_CASE(4) BLTC_PAR_CASE(5) BLTC_PAR_CASE(6)
     BLTC_PAR_CASE(7) BLTC_PAR_CASE(8) BLTC_PAR_CASE(10) BLTC_PAR_CASE(11)
@@ -984,10 +984,10 @@ bool far_packed_dispatch(const EvalArgs& a, const PackedItems& it, int* counter,
     case 9:
       // tuned for the benchmark degree: k2 unrolled by 3, FORM 2 (measured)
       if (tune_form() != 2) far_packed_launch<KIND, 9, 1, 0>(a, it, counter, st);
-      else if (KIND == 1)   // Yukawa: one CTA per SM, full register file (C3 far -4%)
+      else if (KIND == 1)   // Yukawa: one CTA per SM, full register file (C3 far -4%; x9 +10%)
         far_packed_launch<KIND, 9, 3, 2, 1>(a, it, counter, st);
-      else if (tune_far_dy())
-        far_packed_launch<KIND, 9, 3, 2, 2, false, true>(a, it, counter, st);
+      else if (tune_far_dy())   // k2 fully unrolled: C4 far 687 -> 676 ms (x3: 687, x4: 680)
+        far_packed_launch<KIND, 9, 9, 2, 2, false, true>(a, it, counter, st);
       else if (tune_far_unroll(KIND) == 3) far_packed_launch<KIND, 9, 3, 2>(a, it, counter, st);
       else far_packed_launch<KIND, 9, 1, 2>(a, it, counter, st);
       return true;
