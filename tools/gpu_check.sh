@@ -12,6 +12,12 @@ timeout 600 python bench.py --impl reference --steps 2 > gpurun_out/bench_ref.js
 for c in c1 c2 c3 c5; do
   timeout 600 python bench.py --config $c --steps 3 --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
 done
+timeout 900 python bench.py --mode parity --steps 2 --no-cpu-baseline --no-accuracy \
+  > gpurun_out/bench_parity_c4.json 2> gpurun_out/bench_parity_c4.err
+# the paper's Fig. 3 theta x degree sweep through the harness
+timeout 900 python -m paper_2003_01836_b200 sweep --n-particles 1000000 --thetas 0.5,0.7,0.9 \
+  --degrees 1,2,3,4,5,6,7,8,9,10,11,12 --batch-size 160 --verify 4000 --format csv \
+  --output gpurun_out/sweep_fig3_1m.csv > gpurun_out/sweep_fig3.log 2>&1
 # N > 1 flow on one GPU (test hook, not a reported number)
 BLTC_BENCH_SHARE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
   --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 2 --steps 2 --config c2 \
