@@ -968,7 +968,9 @@ bool far_packed_dispatch_parity(const EvalArgs& a, const PackedItems& it, int* c
       // the benchmark degree: one CTA per SM with the full register file and
       // k2 unrolled by 3 -- the IEEE sqrt / division chains want ILP more
       // than warps (C4 far 2151 -> 2054 ms; 2 CTAs per SM spill at 128 regs)
-      far_packed_launch<KIND, 9, 3, 0, 1, true>(a, it, counter, st);   // x9: 2482 ms
+      // dy^2 per (target, k2) in shared memory (the same rounded products):
+      // 2053 -> 2034 ms; k2 x9: 2482 ms
+      far_packed_launch<KIND, 9, 3, 0, 1, true, true>(a, it, counter, st);
       return true;
     BLTC_PAR_CASE(2) BLTC_PAR_CASE(3) BLTC_PAR_CASE(4) BLTC_PAR_CASE(5) BLTC_PAR_CASE(6)
     BLTC_PAR_CASE(7) BLTC_PAR_CASE(8) BLTC_PAR_CASE(10) BLTC_PAR_CASE(11)
