@@ -45,9 +45,16 @@ extern "C" {
  * PARITY: bit-faithful to the reference (IEEE sqrt/div, no FMA, the
  *         reference's per-target accumulation order incl. Neumaier).
  * FAST:   rsqrt + FMA, register-blocked tiles, load-balanced work items;
- *         validated against PARITY / the oracle within tolerances. */
+ *         validated against PARITY / the oracle within tolerances.
+ * STRICT: the default of the Python shim.  Bitwise moments, the FAST
+ *         interaction kernels, and a per-target certificate: every target
+ *         whose FAST value cannot be shown to lie within 0.5e-10 (relative)
+ *         of the reference's is recomputed in the reference's arithmetic
+ *         and order (bitwise).  Result: every target within the north-star
+ *         1e-10 of the reference at FAST speed. */
 #define BLTC_MODE_PARITY 0
 #define BLTC_MODE_FAST 1
+#define BLTC_MODE_STRICT 2
 
 typedef struct bltc_ctx bltc_ctx;
 
@@ -85,6 +92,9 @@ typedef struct {
   int32_t batch_depth;
   int32_t packed;        /* FAST: 1 = packed multi-batch work items, 0 = per-batch chunks */
   int32_t reserved;
+  int64_t n_recomputed;  /* STRICT: targets recomputed in the reference's arithmetic
+                            (-1: evaluated as PARITY throughout) */
+  double strict_s;       /* STRICT: certificate + recompute time */
 } bltc_stats;
 
 BLTC_API const char* bltc_last_error(void);
@@ -151,6 +161,13 @@ BLTC_API int bltc_export_lists(bltc_ctx* ctx, int64_t* a_ptr, int64_t* a_idx, in
                       int64_t* d_idx);
 /* Moments: cluster ids [n_moments] and rows [n_moments][(n+1)^3]. */
 BLTC_API int bltc_export_moments(bltc_ctx* ctx, int64_t* cluster_ids, double* rows);
+/* STRICT certificate of the last single-device run, per target in the
+ * ORIGINAL order: S_i = absum_i + farbound_b (the absolute mass of the pair
+ * terms; the FAST-vs-reference difference is bounded by Kc eps S_i) -- for
+ * calibration and tests.  Needs bltc_strict_keep_bounds(ctx, 1) before the
+ * run; *kc_out: the Kc in use. */
+BLTC_API int bltc_strict_keep_bounds(bltc_ctx* ctx, int32_t enable);
+BLTC_API int bltc_export_strict_bounds(bltc_ctx* ctx, double* bounds_out, double* kc_out);
 
 /* run_distributed (decomp.py:483-593) in one process: R ranks on the given
  * devices (rank r on devices[r % n_devices]), one host thread per rank; the
@@ -284,6 +301,10 @@ BLTC_API int bltc_probe_fp64(int device, double seconds, double* dfma_per_s);
 /* Kernels libbltc has launched in this process so far (all contexts): the
  * benchmark's count of its own launches inside a timed region. */
 BLTC_API int bltc_launch_count(int64_t* out);
+/* exp(x[i]) for i < n with the device port of the host libm exp the
+ * reference's Yukawa tiles call (csrc/libm_exp.cuh); host pointers.  Lets a
+ * test compare the device build with the host's exp bit for bit. */
+BLTC_API int bltc_libm_exp_device(int device, int64_t n, const double* x, double* y);
 
 #ifdef __cplusplus
 }

@@ -19,6 +19,7 @@ BLTC_ERR_STATE = -3
 BLTC_ERR_UNSUPPORTED = -4
 MODE_PARITY = 0
 MODE_FAST = 1
+MODE_STRICT = 2
 
 _f64p = ctypes.POINTER(ctypes.c_double)
 _i64p = ctypes.POINTER(ctypes.c_int64)
@@ -42,7 +43,8 @@ class Stats(ctypes.Structure):
                 ("far_s", ctypes.c_double), ("near_s", ctypes.c_double),
                 ("n_moments", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
                 ("tree_depth", ctypes.c_int32), ("batch_depth", ctypes.c_int32),
-                ("packed", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("packed", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("n_recomputed", ctypes.c_int64), ("strict_s", ctypes.c_double)]
 
 
 class Sizes(ctypes.Structure):
@@ -94,6 +96,9 @@ SIGNATURES = {
                                        ctypes.c_int32, _i64p, ctypes.POINTER(_vp), _vp]),
     "bltc_probe_fp64": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _f64p]),
     "bltc_launch_count": (ctypes.c_int, [_i64p]),
+    "bltc_libm_exp_device": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, _f64p, _f64p]),
+    "bltc_strict_keep_bounds": (ctypes.c_int, [_vp, ctypes.c_int32]),
+    "bltc_export_strict_bounds": (ctypes.c_int, [_vp, _f64p, _f64p]),
     "bltc_run_distributed": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
                                             ctypes.c_int32, ctypes.POINTER(Params), _f64p,
                                             ctypes.c_int64, _f64p, _f64p, _f64p, _f64p, _i64p,

@@ -29,6 +29,12 @@ bool launch_moments_k1(const double* sx, const double* sy, const double* sz, con
                        const int32_t* cstop, const double* lo, const double* hi,
                        const double* s_nodes, const double* w_nodes, int degree, int mstride,
                        double* rows, cudaStream_t st);
+bool launch_moments_bw(const double* sx, const double* sy, const double* sz, const double* sq,
+                       const int32_t* list, int64_t n_list, const int32_t* cstart,
+                       const int32_t* cstop, const double* lo, const double* hi,
+                       const double* s_nodes, const double* w_nodes, int degree, int mstride,
+                       double* rows, DBuf<int32_t>& cnt, DBuf<int32_t>& off, DBuf<int2>& items,
+                       DBuf<int32_t>& scan_tmp, HostScratch& hs, cudaStream_t st);
 __global__ void k_lists(int64_t nb, int G, int g, const double* bcenter, const double* bradius,
                         const int32_t* bstart, const int32_t* bstop, const MacNode* nodes,
                         int32_t cluster_offset, double theta, int64_t per_node, bool fill,
@@ -265,6 +271,10 @@ struct bltc_ctx {
   DBuf<MacNode> f_mac;
   DBuf<double> f_x, f_y, f_z, f_q, f_rows;
   DBuf<double4> f_src4;
+  // STRICT
+  DBuf<double> absum;
+  StrictScratch strict;
+  int64_t n_recomputed = 0;   // -2: count on the device (strict.counters[0]); -1: evaluated as PARITY
 };
 
 namespace {
@@ -298,8 +308,9 @@ void check_params(const bltc_params* p) {
     set_error("kernel_code must be 0, 1 or 2");
     throw UserError{BLTC_ERR_VALUE};
   }
-  if (p->mode != BLTC_MODE_PARITY && p->mode != BLTC_MODE_FAST) {
-    set_error("mode must be BLTC_MODE_PARITY or BLTC_MODE_FAST");
+  if (p->mode != BLTC_MODE_PARITY && p->mode != BLTC_MODE_FAST &&
+      p->mode != BLTC_MODE_STRICT) {
+    set_error("mode must be BLTC_MODE_PARITY, BLTC_MODE_FAST or BLTC_MODE_STRICT");
     throw UserError{BLTC_ERR_VALUE};
   }
 }
@@ -420,6 +431,41 @@ void build_lists(bltc_ctx* c, const bltc_params* p, int G, const MacNode* const*
   }
 }
 
+// Moments of the listed clusters into rows (one row per list entry).  FAST:
+// source pieces with fused products, summed piece by piece; PARITY / STRICT:
+// bitwise the reference's sums (k_moments_bw; the older one-CTA-per-(cluster,
+// k1) and one-CTA-per-cluster kernels remain for degrees 0 and 13-20 and as
+// BLTC_MOMENTS_BW=0 / BLTC_PARITY_MOMENTS_OLD=1 measurement switches).
+void run_moments(bltc_ctx* c, const bltc_params* p, const double* x, const double* y,
+                 const double* z, const double* q, const int32_t* list, int64_t n_list,
+                 const int32_t* start, const int32_t* stop, const double* lo, const double* hi,
+                 int mstride, double* rows) {
+  cudaStream_t st = c->st;
+  if (p->mode == BLTC_MODE_FAST) {
+    launch_moments_split(x, y, z, q, list, n_list, start, stop, lo, hi, c->s_nodes.p,
+                         c->w_nodes.p, p->degree, mstride, rows, c->item_cnt, c->item_off,
+                         c->items, c->partial, c->bs.scan_tmp, c->hs, st);
+    return;
+  }
+  if (launch_moments_bw(x, y, z, q, list, n_list, start, stop, lo, hi, c->s_nodes.p,
+                        c->w_nodes.p, p->degree, mstride, rows, c->item_cnt, c->item_off,
+                        c->items, c->bs.scan_tmp, c->hs, st))
+    return;
+  const int m = p->degree + 1;
+  int threads = ((m * m + 31) / 32) * 32;
+  if (threads < 96) threads = 96;
+  const char* old_env = std::getenv("BLTC_PARITY_MOMENTS_OLD");
+  const bool k1 = !(old_env && std::atoi(old_env) != 0) &&
+                  launch_moments_k1(x, y, z, q, list, n_list, start, stop, lo, hi,
+                                    c->s_nodes.p, c->w_nodes.p, p->degree, mstride, rows, st);
+  if (!k1) {
+    k_moments<<<(unsigned)n_list, threads, 0, st>>>(x, y, z, q, list, start, stop, lo, hi,
+                                                    c->s_nodes.p, c->w_nodes.p, p->degree,
+                                                    mstride, rows);
+    BLTC_LAUNCH_CHECK();
+  }
+}
+
 // Moments of the flagged clusters of one source tree (moments.py:147-150).
 // all: 0 = clusters on some approximation list, 1 = every eligible cluster,
 // 2 = every cluster the MAC could accept (eligible and (n+1)^3 < N_C).
@@ -456,28 +502,9 @@ void compute_moments(bltc_ctx* c, const bltc_params* p, const Partition& T, cons
   k_compact_moments<<<grid_for(nn, 256), 256, 0, st>>>(nn, c->mflag.p, c->mpos.p, c->mlist.p,
                                                        ecl);
   BLTC_LAUNCH_CHECK();
-  if (c->n_moments > 0) {
-    if (p->mode == BLTC_MODE_FAST) {
-      launch_moments_split(T.x.p, T.y.p, T.z.p, T.q.p, c->mlist.p, c->n_moments, T.start.p,
-                           T.stop.p, T.lo.p, T.hi.p, c->s_nodes.p, c->w_nodes.p, p->degree,
-                           mstride, rows.p, c->item_cnt, c->item_off, c->items, c->partial,
-                           c->bs.scan_tmp, c->hs, st);
-    } else {
-      int threads = ((m * m + 31) / 32) * 32;
-      if (threads < 96) threads = 96;
-      const char* old_env = std::getenv("BLTC_PARITY_MOMENTS_OLD");
-      const bool k1 = !(old_env && std::atoi(old_env) != 0) &&
-                      launch_moments_k1(T.x.p, T.y.p, T.z.p, T.q.p, c->mlist.p, c->n_moments,
-                                        T.start.p, T.stop.p, T.lo.p, T.hi.p, c->s_nodes.p,
-                                        c->w_nodes.p, p->degree, mstride, rows.p, st);
-      if (!k1) {
-        k_moments<<<(unsigned)c->n_moments, threads, 0, st>>>(
-            T.x.p, T.y.p, T.z.p, T.q.p, c->mlist.p, T.start.p, T.stop.p, T.lo.p, T.hi.p,
-            c->s_nodes.p, c->w_nodes.p, p->degree, mstride, rows.p);
-        BLTC_LAUNCH_CHECK();
-      }
-    }
-  }
+  if (c->n_moments > 0)
+    run_moments(c, p, T.x.p, T.y.p, T.z.p, T.q.p, c->mlist.p, c->n_moments, T.start.p, T.stop.p,
+                T.lo.p, T.hi.p, mstride, rows.p);
 }
 
 void build_batches(bltc_ctx* c, Partition& T) {
@@ -494,9 +521,16 @@ void build_batches(bltc_ctx* c, Partition& T) {
   BLTC_LAUNCH_CHECK();
 }
 
+// Potentials of the context's targets (sorted order, c->out_sorted) against
+// G source groups.  PARITY: the packed PAR kernels (or k_eval_parity);
+// FAST: the packed FAST kernels (or the per-batch ones); STRICT: FAST with
+// the near field's |term| sums, then strict_fixup certifies every target or
+// recomputes it in the reference's arithmetic (strict.cu).  STRICT without a
+// packed instantiation (constant kernel, degrees 0 and 13-20) evaluates as
+// PARITY -- bitwise, so trivially within the tolerance.
 void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, const double* sx,
               const double* sy, const double* sz, const double* sq, const double4* src4,
-              const double* rows, bltc_stats* stats) {
+              const double* rows, int64_t n_rows, bltc_stats* stats) {
   cudaStream_t st = c->st;
   const Partition& T = *c->tgt;
   EvalArgs a{};
@@ -530,7 +564,12 @@ void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, 
   a.g_lo = 0;
   a.g_hi = G;
   a.par_first = a.par_last = 1;
-  const bool parity_packed = p->mode == BLTC_MODE_PARITY &&
+  const bool strict = p->mode == BLTC_MODE_STRICT &&
+                      packed_supported(p->kernel_code, p->degree);
+  const bool as_parity = p->mode == BLTC_MODE_PARITY ||
+                         (p->mode == BLTC_MODE_STRICT && !strict);
+  c->n_recomputed = as_parity && p->mode == BLTC_MODE_STRICT ? -1 : 0;
+  const bool parity_packed = as_parity &&
                              packed_supported(p->kernel_code, p->degree) &&
                              !(std::getenv("BLTC_PARITY_PACKED") &&
                                std::atoi(std::getenv("BLTC_PARITY_PACKED")) == 0);
@@ -564,7 +603,7 @@ void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, 
       stats->near_s = near_ms * 1e-3;
       stats->packed = 1;
     }
-  } else if (p->mode == BLTC_MODE_PARITY) {
+  } else if (as_parity) {
     launch_eval_parity(a, p->kernel_code, st);
   } else {
     c->far_out.resize(T.n);
@@ -575,9 +614,32 @@ void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, 
       PackedItems pi;
       build_packed_items(a, c->pk_order, c->pk_pc, c->pk_poff, c->pk_wcnt, c->pk_woff, c->pk_items,
                          c->pk_dmask, c->lists.n_direct, c->bs.scan_tmp, c->hs, st, &pi);
-      if (packed_preferred(p->kernel_code, pi.chunk_lane_eff)) {
+      if (strict || packed_preferred(p->kernel_code, pi.chunk_lane_eff)) {
+        if (strict) {
+          c->absum.resize(T.n);
+          a.absum = c->absum.p;
+        }
         launch_eval_packed(a, p->kernel_code, pi, c->counters.p, st, &far_ms, &near_ms,
-                           c->timing);
+                           c->timing, false, strict);
+        if (strict) {
+          cudaEvent_t e0 = nullptr, e1 = nullptr;
+          if (c->timing) {
+            BLTC_CUDA(cudaEventCreate(&e0));
+            BLTC_CUDA(cudaEventCreate(&e1));
+            BLTC_CUDA(cudaEventRecord(e0, st));
+          }
+          strict_fixup(a, p->kernel_code, n_rows, c->strict, T.n, st);
+          c->n_recomputed = -2;   // on the device: read with the stats
+          if (c->timing) {
+            BLTC_CUDA(cudaEventRecord(e1, st));
+            BLTC_CUDA(cudaEventSynchronize(e1));
+            float ms = 0;
+            BLTC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            if (stats) stats->strict_s = ms * 1e-3;
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+          }
+        }
         if (stats) {
           stats->far_s = far_ms * 1e-3;
           stats->near_s = near_ms * 1e-3;
@@ -607,6 +669,17 @@ void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, 
       stats->near_s = near_ms * 1e-3;
     }
   }
+}
+
+// STRICT: targets recomputed in the reference's arithmetic by the last
+// evaluation (-1: evaluated as PARITY; 0 otherwise).  Synchronises.
+int64_t read_recomputed(bltc_ctx* c) {
+  if (c->n_recomputed != -2) return c->n_recomputed;
+  int32_t* h = (int32_t*)c->hs.get(64);
+  BLTC_CUDA(cudaMemcpyAsync(h, c->strict.counters.p, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                            c->st));
+  BLTC_CUDA(cudaStreamSynchronize(c->st));
+  return h[0];
 }
 
 // BLTC_TRACE=1: synchronise and print host wall time per pipeline stage.
@@ -692,7 +765,7 @@ void run_pipeline(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64
     BLTC_LAUNCH_CHECK();
   }
   evaluate(c, p, 1, c->ecl.p, c->src.x.p, c->src.y.p, c->src.z.p, c->src.q.p, c->src4.p,
-           c->rows.p, stats);
+           c->rows.p, c->n_moments, stats);
   k_unpermute<<<grid_for(n_t, 256), 256, 0, st>>>(n_t, c->out_sorted.p, c->tgt->perm.p, phi_dev);
   BLTC_LAUNCH_CHECK();
   tr("evaluate");
@@ -715,6 +788,7 @@ void run_pipeline(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64
     stats->kernel_launches = g_launch_count - launches0;
     stats->tree_depth = c->src.depth;
     stats->batch_depth = c->tgt->depth;
+    stats->n_recomputed = read_recomputed(c);
   } else {
     BLTC_CUDA(cudaStreamSynchronize(st));
   }
@@ -1071,6 +1145,38 @@ int bltc_export_moments(bltc_ctx* c, int64_t* cluster_ids, double* rows) {
   });
 }
 
+int bltc_strict_keep_bounds(bltc_ctx* c, int32_t enable) {
+  return guarded([&] {
+    if (!c) {
+      set_error("ctx is NULL");
+      throw UserError{BLTC_ERR_VALUE};
+    }
+    c->strict.want_bounds = enable != 0;
+  });
+}
+
+int bltc_export_strict_bounds(bltc_ctx* c, double* bounds_out, double* kc_out) {
+  return guarded([&] {
+    require_run(c);
+    if (kc_out) *kc_out = strict_kc();
+    if (c->n_recomputed != -2 || !c->strict.want_bounds || c->rank_built) {
+      set_error("no STRICT single-device run with bltc_strict_keep_bounds enabled");
+      throw UserError{BLTC_ERR_STATE};
+    }
+    BLTC_CUDA(cudaSetDevice(c->device));
+    const int64_t n = c->tgt->n;
+    if (bounds_out && n > 0) {
+      c->phi_dev.resize(n);
+      k_unpermute<<<grid_for(n, 256), 256, 0, c->st>>>(n, c->strict.bounds.p, c->tgt->perm.p,
+                                                       c->phi_dev.p);
+      BLTC_LAUNCH_CHECK();
+      BLTC_CUDA(cudaMemcpyAsync(bounds_out, c->phi_dev.p, n * sizeof(double),
+                                cudaMemcpyDeviceToHost, c->st));
+    }
+    BLTC_CUDA(cudaStreamSynchronize(c->st));
+  });
+}
+
 int bltc_direct_sum(bltc_ctx* c, int32_t kernel_code, double kappa, int32_t mode,
                     int64_t n_idx, const int64_t* idx, int64_t n_t, const double* tx,
                     const double* ty, const double* tz, int64_t n_s, const double* sx,
@@ -1367,7 +1473,7 @@ int bltc_rank_evaluate(bltc_ctx* c, const bltc_params* p, int32_t ranks, int32_t
       BLTC_LAUNCH_CHECK();
     }
     evaluate(c, p, G, c->f_ecl.p, c->f_x.p, c->f_y.p, c->f_z.p, c->f_q.p, c->f_src4.p,
-             c->f_rows.p, stats);
+             c->f_rows.p, RW, stats);
     const int64_t n = c->rank_n;
     c->phi_dev.resize(n);
     k_unpermute<<<grid_for(n, 256), 256, 0, st>>>(n, c->out_sorted.p, c->tgt->perm.p,
@@ -1393,6 +1499,7 @@ int bltc_rank_evaluate(bltc_ctx* c, const bltc_params* p, int32_t ranks, int32_t
       stats->kernel_launches = g_launch_count - launches0;
       stats->tree_depth = c->src.depth;
       stats->batch_depth = c->tgt->depth;
+      stats->n_recomputed = read_recomputed(c);
     }
     c->have_run = true;
   });
@@ -1486,23 +1593,8 @@ int bltc_stage_moments(bltc_ctx* c, const bltc_params* p, const double* cheb_s, 
     const int64_t m3 = (int64_t)m * m * m;
     const int mstride = moment_stride(p->degree);
     c->rows.resize(n_list * mstride + 2);
-    if (p->mode == BLTC_MODE_FAST) {
-      launch_moments_split(S.x.p, S.y.p, S.z.p, S.q.p, c->mlist.p, n_list, S.start.p, S.stop.p,
-                           S.lo.p, S.hi.p, c->s_nodes.p, c->w_nodes.p, p->degree, mstride,
-                           c->rows.p, c->item_cnt, c->item_off, c->items, c->partial,
-                           c->bs.scan_tmp, c->hs, st);
-    } else {
-      int threads = ((m * m + 31) / 32) * 32;
-      if (threads < 96) threads = 96;
-      if (!launch_moments_k1(S.x.p, S.y.p, S.z.p, S.q.p, c->mlist.p, n_list, S.start.p,
-                             S.stop.p, S.lo.p, S.hi.p, c->s_nodes.p, c->w_nodes.p, p->degree,
-                             mstride, c->rows.p, st))
-        k_moments<<<(unsigned)n_list, threads, 0, st>>>(S.x.p, S.y.p, S.z.p, S.q.p, c->mlist.p,
-                                                        S.start.p, S.stop.p, S.lo.p, S.hi.p,
-                                                        c->s_nodes.p, c->w_nodes.p, p->degree,
-                                                        mstride, c->rows.p);
-      BLTC_LAUNCH_CHECK();
-    }
+    run_moments(c, p, S.x.p, S.y.p, S.z.p, S.q.p, c->mlist.p, n_list, S.start.p, S.stop.p,
+                S.lo.p, S.hi.p, mstride, c->rows.p);
     BLTC_CUDA(cudaMemcpy2DAsync(rows_out, m3 * sizeof(double), c->rows.p,
                                 mstride * sizeof(double), m3 * sizeof(double), n_list,
                                 cudaMemcpyDeviceToHost, st));
@@ -1637,7 +1729,8 @@ int bltc_stage_potentials(bltc_ctx* c, const bltc_params* p, const double* cheb_
       BLTC_LAUNCH_CHECK();
     }
     tm.mark();
-    evaluate(c, p, 1, c->ecl.p, S.x.p, S.y.p, S.z.p, S.q.p, c->src4.p, c->rows.p, stats);
+    evaluate(c, p, 1, c->ecl.p, S.x.p, S.y.p, S.z.p, S.q.p, c->src4.p, c->rows.p, n_rows,
+             stats);
     c->phi_dev.resize(n_t);
     if (perm) {   // (out + carry)[perm] of compute_potentials (engine.py:335)
       h2d_narrow(T.perm, perm, n_t, st, "perm");
@@ -1661,6 +1754,7 @@ int bltc_stage_potentials(bltc_ctx* c, const bltc_params* p, const double* cheb_
       stats->total_s = tm.secs(0, 2);
       stats->n_moments = n_rows;
       stats->kernel_launches = g_launch_count - launches0;
+      stats->n_recomputed = read_recomputed(c);
     }
   });
 }

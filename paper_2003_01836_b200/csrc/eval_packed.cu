@@ -86,13 +86,31 @@ __device__ __forceinline__ double pair_acc(double acc, double q, double d2, cons
   return fma(__dmul_rn(q, ex), y, acc);
 }
 
+// The FAST kernel factor f with term = q f (FORM 2): Coulomb y0 p, Yukawa
+// exp(-kappa r) y -- the same roundings as pair_acc<KIND, 2>.  STRICT's near
+// field accumulates both q f and |q| f.
+template <int KIND>
+__device__ __forceinline__ double pair_factor(double d2, const YukawaK& yk) {
+  if (KIND == 0) {
+    double y0;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(d2));
+    const double e = fma(-__dmul_rn(d2, y0), y0, 1.0);
+    const double c = fma(0.375, e, 0.5);
+    const double p = fma(e, c, 1.0);
+    return __dmul_rn(y0, p);
+  }
+  const double y = rsqrt_fast(d2);
+  const double r = __dmul_rn(d2, y);
+  return __dmul_rn(exp_neg_kr(r, yk), y);
+}
+
 // PARITY: the reference tiles' term, IEEE sqrt / division, no contraction
 // (engine.py:183-191, 240-244).
 template <int KIND>
 __device__ __forceinline__ double parity_term(double q, double d2, double kappa) {
   if (KIND == 0) return __ddiv_rn(q, __dsqrt_rn(d2));
   const double r = __dsqrt_rn(d2);
-  return __ddiv_rn(__dmul_rn(exp(__dmul_rn(-kappa, r)), q), r);
+  return __ddiv_rn(__dmul_rn(libm_exp(__dmul_rn(-kappa, r)), q), r);
 }
 
 // Coulomb PARITY term q / sqrt(d2) on the intrinsics' fast paths (bitwise
@@ -540,10 +558,11 @@ constexpr int kNearUnroll = BLTC_NEAR_UNROLL;   // pragma arguments are not macr
 // kFoldChunks chunks of 32 sources (C4 near 206.0 ms folding every chunk,
 // 204.3 every 2, 203.4 every 4, 202.7 every 8)
 constexpr int kFoldChunks = BLTC_FOLD_CHUNKS;
-template <int KIND, int CH, bool MASKED, int FORM>
-__device__ __forceinline__ void near_chunk(double (&part)[2], const double4* src,
-                                           const double (&tx)[2], const double (&ty)[2],
-                                           const double (&tz)[2], const YukawaK& yk) {
+template <int KIND, int CH, bool MASKED, int FORM, bool ABS = false>
+__device__ __forceinline__ void near_chunk(double (&part)[2], double (&apart)[2],
+                                           const double4* src, const double (&tx)[2],
+                                           const double (&ty)[2], const double (&tz)[2],
+                                           const YukawaK& yk) {
   const long long tb = __double_as_longlong(kSingularSq);   // d2 >= 0: bit order = value order
 #pragma unroll kNearUnroll
   for (int j = 0; j < CH; ++j) {
@@ -553,15 +572,23 @@ __device__ __forceinline__ void near_chunk(double (&part)[2], const double4* src
       const double dx = __dsub_rn(tx[t], s.x);
       const double dy = __dsub_rn(ty[t], s.y);
       const double dz = __dsub_rn(tz[t], s.z);
+      double d2, q;
       if (MASKED) {
         // d2 + 1e-300: exactly d2 for every non-singular pair, never 0, so
         // only the charge needs the select (excluded pairs add 0 * finite)
-        const double d2 = fma(dz, dz, fma(dy, dy, fma(dx, dx, 1e-300)));
+        d2 = fma(dz, dz, fma(dy, dy, fma(dx, dx, 1e-300)));
         const bool ok = __double_as_longlong(d2) >= tb;
-        part[t] = pair_acc<KIND, FORM>(part[t], ok ? s.w : 0.0, d2, yk);
+        q = ok ? s.w : 0.0;
       } else {
-        const double d2 = fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx)));
-        part[t] = pair_acc<KIND, FORM>(part[t], s.w, d2, yk);
+        d2 = fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx)));
+        q = s.w;
+      }
+      if (ABS) {
+        const double f = pair_factor<KIND>(d2, yk);
+        part[t] = fma(q, f, part[t]);
+        apart[t] = fma(fabs(q), f, apart[t]);
+      } else {
+        part[t] = pair_acc<KIND, FORM>(part[t], q, d2, yk);
       }
     }
   }
@@ -766,7 +793,7 @@ __device__ __forceinline__ bool near_stage_bulk(const EvalArgs& a, const uint8_t
 // per-pair Neumaier compensation, out = acc + carry at the end (engine.py:
 // 302-312, 335); over several source groups one pass per group, (acc, carry)
 // handed from pass to pass (decomp.py:437-454).
-template <int KIND, int CH, int FORM, bool PAR = false, bool BULK = false>
+template <int KIND, int CH, int FORM, bool PAR = false, bool BULK = false, bool ABS = false>
 __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 it,
                                                  const int32_t* poff, const uint8_t* dmask,
                                                  double4* wsm, int lane, uint64_t* bar,
@@ -798,6 +825,7 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
   }
   const double4* mine = wsm + L.g * NearSmem<CH>::kSeg;
   double npart[2] = {0.0, 0.0};   // FAST: partial sum over the last chunks
+  double apart[2] = {0.0, 0.0};   // ABS (STRICT): sum of |q f| over the pairs
   int nchunk = 0;
   bool live = false;
 #pragma unroll
@@ -850,9 +878,10 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
         }
       } else {
         if (masked)
-          near_chunk<KIND, CH, true, FORM>(npart, mine + buf * CH, tx, ty, tz, a.yk);
+          near_chunk<KIND, CH, true, FORM, ABS>(npart, apart, mine + buf * CH, tx, ty, tz, a.yk);
         else
-          near_chunk<KIND, CH, false, FORM>(npart, mine + buf * CH, tx, ty, tz, a.yk);
+          near_chunk<KIND, CH, false, FORM, ABS>(npart, apart, mine + buf * CH, tx, ty, tz,
+                                                 a.yk);
         if ((++nchunk & (kFoldChunks - 1)) == 0 || !more) {   // fold every kFoldChunks chunks
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
@@ -884,6 +913,10 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
     if (L.v1) a.out[L.i1] = __dadd_rn(acc[1], comp[1]);
     return;
   }
+  if (ABS) {
+    if (L.v0) a.absum[L.i0] = apart[0];
+    if (L.v1) a.absum[L.i1] = apart[1];
+  }
   if (L.v0) {
     double total = acc[0], cmp = comp[0];
     neumaier(total, cmp, a.far_out[L.i0]);
@@ -896,7 +929,8 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
   }
 }
 
-template <int KIND, int CH, int MINB, int FORM, bool PAR = false, bool BULK = false>
+template <int KIND, int CH, int MINB, int FORM, bool PAR = false, bool BULK = false,
+          bool ABS = false>
 __global__ void __launch_bounds__(kWarps * 32, MINB)
 k_near_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int32_t* poff,
               const uint8_t* dmask, int* counter) {
@@ -912,7 +946,7 @@ k_near_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int
   __syncwarp();
   unsigned phase = 0;
   for (int item = next_item(counter); item < n_items; item = next_item(counter))
-    near_packed_item<KIND, CH, FORM, PAR, BULK>(a, items[item], poff, dmask, wsm, lane,
+    near_packed_item<KIND, CH, FORM, PAR, BULK, ABS>(a, items[item], poff, dmask, wsm, lane,
                                                 nbar[warp], phase);
 }
 
@@ -1010,12 +1044,12 @@ bool far_packed_dispatch(const EvalArgs& a, const PackedItems& it, int* counter,
   }
 }
 
-template <int KIND, int CH = kNearCh, int FORM = 0, bool PAR = false>
+template <int KIND, int CH = kNearCh, int FORM = 0, bool PAR = false, bool ABS = false>
 void near_packed_launch(const EvalArgs& a, const PackedItems& it, int* counter,
                         cudaStream_t st) {
   const size_t smem = sizeof(double4) * kWarps * NearSmem<CH>::kWarp;
-  auto kern = tune_near_bulk() ? k_near_packed<KIND, CH, 2, FORM, PAR, true>
-                               : k_near_packed<KIND, CH, 2, FORM, PAR, false>;
+  auto kern = tune_near_bulk() ? k_near_packed<KIND, CH, 2, FORM, PAR, true, ABS>
+                               : k_near_packed<KIND, CH, 2, FORM, PAR, false, ABS>;
   BLTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = persistent_grid(kern, kWarps * 32, smem);
   kern<<<grid, kWarps * 32, smem, st>>>(a, it.items_near, it.n_items, it.poff, it.dmask,
@@ -1164,7 +1198,7 @@ void build_packed_items(const EvalArgs& a, PackedOrder& order, DBuf<int32_t>& pc
 
 void launch_eval_packed(const EvalArgs& a, int kind, const PackedItems& it, int* counters,
                         cudaStream_t st, float* far_ms, float* near_ms, bool timing,
-                        bool parity) {
+                        bool parity, bool strict) {
   if (a.nb == 0) return;
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
   if (timing) {
@@ -1186,6 +1220,9 @@ void launch_eval_packed(const EvalArgs& a, int kind, const PackedItems& it, int*
   if (parity) {
     if (kind == 0) near_packed_launch<0, kNearCh, 0, true>(a, it, counters + 1, st);
     else near_packed_launch<1, kNearCh, 0, true>(a, it, counters + 1, st);
+  } else if (strict) {   // FORM 2 arithmetic plus the |term| sums
+    if (kind == 0) near_packed_launch<0, kNearCh, 2, false, true>(a, it, counters + 1, st);
+    else near_packed_launch<1, kNearCh, 2, false, true>(a, it, counters + 1, st);
   } else if (tune_form() != 2) {
     if (kind == 0) near_packed_launch<0>(a, it, counters + 1, st);
     else near_packed_launch<1>(a, it, counters + 1, st);

@@ -24,7 +24,7 @@ __device__ __forceinline__ double parity_term(double q, double d2, double kappa)
   if (KIND == 0) return __ddiv_rn(q, __dsqrt_rn(d2));
   if (KIND == 1) {
     double r = __dsqrt_rn(d2);
-    return __ddiv_rn(__dmul_rn(exp(__dmul_rn(-kappa, r)), q), r);
+    return __ddiv_rn(__dmul_rn(libm_exp(__dmul_rn(-kappa, r)), q), r);
   }
   return q;
 }

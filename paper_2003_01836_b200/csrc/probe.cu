@@ -1,6 +1,7 @@
 // FP64-pipe roofline denominator, measured live: sustained DFMA throughput of
 // the device (MEASURED_PEAKS.json carries HBM and bf16 peaks only).
 #include "bltc_internal.cuh"
+#include "libm_exp.cuh"
 
 namespace bltc {
 namespace {
@@ -19,6 +20,10 @@ __global__ void k_dfma_loop(double* out, int iters, double a, double b) {
 #pragma unroll
   for (int k = 0; k < 8; ++k) s += r[k];
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void k_libm_exp(int64_t n, const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) y[i] = libm_exp(x[i]);
 }
 }  // namespace
 }  // namespace bltc
@@ -68,4 +73,26 @@ extern "C" BLTC_API int bltc_launch_count(int64_t* out) {
   if (!out) return BLTC_ERR_VALUE;
   *out = (int64_t)bltc::g_launch_count;
   return BLTC_OK;
+}
+
+extern "C" BLTC_API int bltc_libm_exp_device(int device, int64_t n, const double* x, double* y) {
+  using namespace bltc;
+  try {
+    if (n < 0 || (n > 0 && (!x || !y))) {
+      set_error("bltc_libm_exp_device: bad arguments");
+      return BLTC_ERR_VALUE;
+    }
+    if (n == 0) return BLTC_OK;
+    if (device >= 0) BLTC_CUDA(cudaSetDevice(device));
+    double* d = nullptr;
+    BLTC_CUDA(cudaMalloc(&d, 2 * n * sizeof(double)));
+    BLTC_CUDA(cudaMemcpy(d, x, n * sizeof(double), cudaMemcpyHostToDevice));
+    k_libm_exp<<<(int)((n + 255) / 256), 256>>>(n, d, d + n);
+    BLTC_LAUNCH_CHECK();
+    BLTC_CUDA(cudaMemcpy(y, d + n, n * sizeof(double), cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    return BLTC_OK;
+  } catch (const CudaFailure&) {
+    return BLTC_ERR_CUDA;
+  }
 }

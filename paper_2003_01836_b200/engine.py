@@ -13,9 +13,15 @@ reference's own object (duck typed: ``targets``/``sources`` with float64
 ``x, y, z``; ``charges``; ``targets is sources`` means coincident).
 ``config`` may be this package's :class:`EvalConfig` or the reference's.
 
-Modes: ``"parity"`` reproduces the reference bit for bit (IEEE sqrt/div, no
-FMA, reference accumulation order); ``"fast"`` is the performance path
-(rsqrt + FMA, register-blocked tiles) validated against it.
+Modes: ``"strict"`` (the default) runs the performance kernels on the
+reference's own moments and certifies every target: a target whose FAST
+value cannot be shown to lie within 0.5e-10 (relative) of the reference's is
+recomputed in the reference's arithmetic, so every potential meets the
+north-star 1e-10 per-target tolerance (``RunStats.n_recomputed`` counts the
+recomputed ones).  ``"parity"`` reproduces the reference bit for bit for
+every target (IEEE sqrt/div, no FMA, reference accumulation order);
+``"fast"`` is the uncertified performance path (rsqrt + FMA, register-blocked
+tiles, FMA-fused moments), within ~1e-13 of max|phi| of the reference.
 """
 from __future__ import annotations
 
@@ -29,8 +35,8 @@ from . import _lib
 from .kernels import KernelSpec, coulomb
 from .particles import ParticleSystem
 
-DEFAULT_MODE = os.environ.get("BLTC_MODE", "fast")
-_MODES = {"parity": _lib.MODE_PARITY, "fast": _lib.MODE_FAST}
+DEFAULT_MODE = os.environ.get("BLTC_MODE", "strict")
+_MODES = {"parity": _lib.MODE_PARITY, "fast": _lib.MODE_FAST, "strict": _lib.MODE_STRICT}
 
 
 @dataclass(frozen=True)
@@ -73,6 +79,8 @@ class RunStats:
     tree_depth: int = 0
     batch_depth: int = 0
     packed: int = 0
+    n_recomputed: int = 0
+    strict_s: float = 0.0
 
     @classmethod
     def from_c(cls, s: _lib.Stats) -> "RunStats":
@@ -313,6 +321,21 @@ class Context:
                                                _lib.i64p(out["a_idx"]), _lib.i64p(out["d_ptr"]),
                                                _lib.i64p(out["d_idx"])))
         return out
+
+    def keep_strict_bounds(self, enable: bool = True) -> None:
+        """Keep the STRICT certificate's per-target bound of the next runs."""
+        _lib.check(self._lib.bltc_strict_keep_bounds(self.handle, 1 if enable else 0))
+
+    def export_strict_bounds(self) -> tuple[np.ndarray, float]:
+        """(S, Kc) of the last STRICT run: S_i = absum_i + farbound_i per target
+        in the original order; a target is certified when Kc eps S_i <= 0.5e-10
+        |phi_i| and recomputed in the reference's arithmetic otherwise."""
+        n = self.sizes().n_targets
+        out = np.empty(n)
+        kc = ctypes.c_double()
+        _lib.check(self._lib.bltc_export_strict_bounds(self.handle, _lib.f64p(out),
+                                                       ctypes.byref(kc)))
+        return out, kc.value
 
     def export_moments(self):
         sz = self.sizes()

@@ -38,8 +38,7 @@ def test_simulated_ranks_match_reference(bltc, case, mode):
     g = golden(case)
     s = golden_system(g)
     phi, st = run_distributed(s, _cfg(bltc, g), ranks=int(g["ranks"]), mode=mode)
-    exact = mode == "parity" and int(g["kind"]) == 0
-    _check(phi, g["phi"], exact, 1e-14 if mode == "parity" else 1e-13)
+    _check(phi, g["phi"], mode == "parity", 1e-13)
     assert st.direct_pairs == int(g["direct_pairs"])
     assert st.approx_pairs == int(g["approx_pairs"])
 
@@ -132,8 +131,7 @@ def test_c_run_distributed_matches_reference(bltc, case, mode):
     s = golden_system(g)
     phi, st = run_distributed_native(s, _cfg(bltc, g), ranks=int(g["ranks"]), devices=[0],
                                      mode=mode)
-    exact = mode == "parity" and int(g["kind"]) == 0
-    _check(phi, g["phi"], exact, 1e-14 if mode == "parity" else 1e-13)
+    _check(phi, g["phi"], mode == "parity", 1e-13)
     assert st.direct_pairs == int(g["direct_pairs"])
     assert st.approx_pairs == int(g["approx_pairs"])
     np.testing.assert_array_equal(st.rank_counts, np.diff(g["rank_start"]))

@@ -65,15 +65,11 @@ def test_process_group_ranks_match_reference(tmp_path, case):
     R = int(g["ranks"])
     mp.start_processes(_worker, args=(R, _free_port(), case, str(tmp_path)), nprocs=R,
                        join=True, start_method="spawn")
-    exact = int(g["kind"]) == 0
     part = rcb_partition(golden_system(g).sources, R)
     for r in range(R):
         for ex in ("let", "replicate"):
             phi = np.load(tmp_path / f"phi_{ex}{r}.npy")
-            if exact:
-                np.testing.assert_array_equal(phi, g["phi"])
-            else:
-                assert np.abs(phi - g["phi"]).max() <= 1e-14 * np.abs(g["phi"]).max()
+            np.testing.assert_array_equal(phi, g["phi"])
             pairs = np.load(tmp_path / f"pairs_{ex}{r}.npy")
             assert (int(pairs[0]), int(pairs[1])) == (int(g["direct_pairs"]),
                                                       int(g["approx_pairs"]))

@@ -1,0 +1,162 @@
+"""STRICT mode (csrc/strict.cu): the FAST kernels on the reference's own
+moments, every target certified within 0.5e-10 of the reference or
+recomputed in the reference's arithmetic.  The bar is the north star's, on
+EVERY target (no masking of near-cancelling ones): |phi_i - ref_i| <=
+1e-10 |ref_i| (ref_i = 0 -> phi_i = 0).  Forcing the recompute of every
+target (BLTC_STRICT_KC=1e300) must give the reference bit for bit."""
+import math
+
+import numpy as np
+import pytest
+from conftest import golden, golden_system
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["c1_coulomb", "small_yukawa", "plummer", "deg8"]
+
+
+@pytest.fixture(scope="module")
+def bltc():
+    import paper_2003_01836_b200 as pkg
+    pkg._lib.load()
+    return pkg
+
+
+def _config(bltc, g):
+    kind = int(g["kind"])
+    kernel = [bltc.coulomb(), bltc.yukawa(float(g["kappa"])), bltc.test_constant()][kind]
+    return bltc.EvalConfig(theta=float(g["theta"]), degree=int(g["degree"]),
+                           leaf_size=int(g["leaf"]), batch_size=int(g["batch"]), kernel=kernel)
+
+
+def strict_ok(phi, ref, tol=1e-10):
+    d = np.abs(phi - ref)
+    bad = ~(d <= tol * np.abs(ref))
+    assert not bad.any(), (f"{int(bad.sum())} targets above {tol}: worst rel "
+                           f"{(d[bad] / np.abs(ref[bad])).max():.3e}")
+
+
+def test_device_exp_is_host_libm_bitwise(bltc):
+    import ctypes
+    rng = np.random.default_rng(3)
+    x = np.concatenate([rng.uniform(-1100, 1100, 100_000), -0.5 * np.sqrt(rng.uniform(0, 3, 100_000)),
+                        -np.exp(rng.uniform(-60, 6, 50_000)),
+                        [0.0, -0.0, 1e-300, -745.2, -708.5, 709.9, -np.inf, np.inf, np.nan]])
+    y = np.empty_like(x)
+    lib = bltc._lib.load()
+    bltc._lib.check(lib.bltc_libm_exp_device(0, x.shape[0], bltc._lib.f64p(x), bltc._lib.f64p(y)))
+    host = np.array([math.exp(v) if v < 709.8 else (math.inf if v == v else math.nan)
+                     for v in x])
+    same = (y.view(np.uint64) == host.view(np.uint64)) | (np.isnan(y) & np.isnan(host))
+    assert same.all(), x[~same][:5]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_strict_every_target_within_1e10(bltc, case):
+    g = golden(case)
+    phi, st = bltc.treecode_potentials(golden_system(g), _config(bltc, g), mode="strict")
+    strict_ok(phi, g["phi"])
+    assert st.direct_pairs == int(g["direct_pairs"])
+    assert st.approx_pairs == int(g["approx_pairs"])
+    assert st.n_recomputed >= 0
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_strict_forced_recompute_is_reference_bitwise(bltc, case, monkeypatch):
+    g = golden(case)
+    monkeypatch.setenv("BLTC_STRICT_KC", "1e300")
+    phi, st = bltc.treecode_potentials(golden_system(g), _config(bltc, g), mode="strict")
+    np.testing.assert_array_equal(phi, g["phi"])
+    assert st.n_recomputed == phi.shape[0]
+
+
+def test_strict_kc_zero_recomputes_nothing(bltc, monkeypatch):
+    """Kc = 0: the certificate passes everything; the result is the FAST
+    kernels' on the reference's moments (never further than FAST mode)."""
+    g = golden("plummer")
+    s, cfg = golden_system(g), _config(bltc, g)
+    monkeypatch.setenv("BLTC_STRICT_KC", "0")
+    phi, st = bltc.treecode_potentials(s, cfg, mode="strict")
+    assert st.n_recomputed == 0
+    ref = g["phi"]
+    assert np.abs(phi - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("gen,n,leaf,batch,deg,theta,kind", [
+    ("uniform", 200_000, 2000, 160, 8, 0.8, 0),
+    ("plummer", 200_000, 2000, 160, 8, 0.8, 0),
+    ("uniform", 150_000, 2000, 160, 10, 0.7, 0),
+    ("uniform", 150_000, 2000, 160, 8, 0.8, 1),
+])
+def test_strict_mid_size_vs_oracle(bltc, oracle, gen, n, leaf, batch, deg, theta, kind):
+    import os
+    from paper_2003_01836_b200 import cli
+    s = (cli.generate_particles if gen == "uniform" else cli.generate_plummer)(n, 4)
+    src = s.sources
+    kappa = 0.5 if kind == 1 else 0.0
+    ref, _ = oracle.treecode_potentials(src.x, src.y, src.z, src.x, src.y, src.z, s.charges,
+                                        True, theta, deg, leaf, batch, kind, kappa,
+                                        threads=os.cpu_count() or 1)
+    kernel = bltc.yukawa(kappa) if kind == 1 else bltc.coulomb()
+    cfg = bltc.EvalConfig(theta=theta, degree=deg, leaf_size=leaf, batch_size=batch,
+                          kernel=kernel)
+    phi, st = bltc.treecode_potentials(s, cfg, mode="strict")
+    strict_ok(phi, ref)
+    phi_p, _ = bltc.treecode_potentials(s, cfg, mode="parity")
+    np.testing.assert_array_equal(phi_p, ref)
+
+
+@pytest.mark.parametrize("deg", [1, 2, 3, 5, 7, 9, 11, 12])
+def test_strict_packed_degrees(bltc, deg):
+    from paper_2003_01836_b200 import cli
+    s = cli.generate_particles(8000, 29)
+    cfg = bltc.EvalConfig(theta=0.75, degree=deg, leaf_size=400, batch_size=100)
+    ref, _ = bltc.treecode_potentials(s, cfg, mode="parity")
+    phi, st = bltc.treecode_potentials(s, cfg, mode="strict")
+    strict_ok(phi, ref)
+    assert st.n_recomputed >= 0
+
+
+@pytest.mark.parametrize("deg,kernel", [(0, "coulomb"), (14, "coulomb"), (3, "const")])
+def test_strict_without_packed_kernels_is_parity(bltc, deg, kernel):
+    from paper_2003_01836_b200 import cli
+    s = cli.generate_particles(3000, 7)
+    k = bltc.coulomb() if kernel == "coulomb" else bltc.test_constant()
+    cfg = bltc.EvalConfig(theta=0.8, degree=deg, leaf_size=200, batch_size=200, kernel=k)
+    ref, _ = bltc.treecode_potentials(s, cfg, mode="parity")
+    phi, st = bltc.treecode_potentials(s, cfg, mode="strict")
+    np.testing.assert_array_equal(phi, ref)
+    assert st.n_recomputed == -1
+
+
+def test_strict_near_cancelling_targets_recomputed(bltc):
+    """Charges +-1 in mirror pairs about the origin: targets on the mirror
+    plane x = 0 have phi ~ 0 (massive cancellation).  STRICT recomputes them
+    and meets the per-target bar; FAST alone does not promise it."""
+    rng = np.random.default_rng(11)
+    n = 30_000
+    p = rng.uniform(-1, 1, (n, 3))
+    p[:, 0] = np.abs(p[:, 0]) + 1e-3
+    q = rng.uniform(0.5, 1.0, n)
+    mirror = p * np.array([-1.0, 1.0, 1.0])
+    plane = np.column_stack([np.zeros(2000), rng.uniform(-1, 1, (2000, 2))])
+    pts = np.concatenate([p, mirror, plane])
+    qs = np.concatenate([q, -q, np.zeros(2000)])
+    system = bltc.ParticleSystem.from_single_set(bltc.Points.from_array(pts), qs)
+    cfg = bltc.EvalConfig(theta=0.8, degree=8, leaf_size=500, batch_size=160)
+    ref, _ = bltc.treecode_potentials(system, cfg, mode="parity")
+    phi, st = bltc.treecode_potentials(system, cfg, mode="strict")
+    strict_ok(phi, ref)
+    assert st.n_recomputed >= 1
+
+
+@pytest.mark.parametrize("case", ["dist_r3", "dist_r4_yukawa"])
+def test_strict_distributed_ranks(bltc, case, monkeypatch):
+    from paper_2003_01836_b200.decomp import run_distributed
+    g = golden(case)
+    s = golden_system(g)
+    phi, st = run_distributed(s, _config(bltc, g), ranks=int(g["ranks"]), mode="strict")
+    strict_ok(phi, g["phi"])
+    monkeypatch.setenv("BLTC_STRICT_KC", "1e300")
+    phi, st = run_distributed(s, _config(bltc, g), ranks=int(g["ranks"]), mode="strict")
+    np.testing.assert_array_equal(phi, g["phi"])
