@@ -2,17 +2,20 @@
 """BLTC evaluation benchmark (BASELINE.json metric) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4]
-                    [--impl ours|reference] [--mode fast|parity]
+                    [--impl ours|reference] [--mode strict|fast|parity]
 
 One step = one full BLTC evaluation of the workload (source tree, target
 batches, interaction lists, moments, far + near field, un-permute) through
-libbltc's CUDA kernels, inputs resident in HBM.  ``value`` is particles/s
-over all ranks; ``e2e`` is the same metric through the public API with
-host (pinned) buffers, H2D/D2H inside the timed region.  ``roofline`` is the
-dominant kernel's (far field) FP64 throughput against the device's FP64 FMA
-peak measured live in the same process.  ``cpu_baseline`` is the CPU
-restatement of the reference algorithm (oracle/, "port") on the host cores
-on a bounded sample.
+libbltc's CUDA kernels, inputs resident in HBM, in the shipped default mode
+STRICT (every target within 1e-10 of the reference: FAST kernels on the
+reference's moments, near-cancelling targets recomputed in the reference's
+arithmetic).  ``value`` is particles/s over all ranks; ``e2e`` is the same
+metric through the public API with host buffers, H2D/D2H inside the timed
+region.  ``roofline`` is the dominant kernel's (far field) FP64 throughput
+against the nominal FP64 peak at the SM clock sampled during the timed
+region (148 SMs x 64 FP64 lanes x 2 flop x f_SM).  ``cpu_baseline`` is the
+CPU restatement of the reference algorithm (oracle/, "port") on the host
+cores on a bounded sample, extrapolated by pair count.
 
 N > 1 (torchrun, one rank per GPU): targets are partitioned by recursive
 coordinate bisection (decomp.py:76-130), each rank builds its tree and
@@ -228,7 +231,8 @@ class CpuReference:
         t = time.perf_counter() - t0
         est = self.setup_s + self.moments_s + t / self.frac
         return {"value": self.system.n_targets / est, "unit": "particles/s",
-                "cores": self.threads, "kind": "port",
+                "cores": self.threads, "kind": "port", "extrapolated": True,
+                "cpu_model": cpu_model(), "sampled_pair_fraction": self.frac,
                 "sample": (f"oracle/ C port of the reference path on {self.threads} host threads: "
                            f"tree+batches+lists {self.setup_s:.1f}s (serial, as in the "
                            f"reference) and moments {self.moments_s:.1f}s measured in full; "
@@ -256,6 +260,17 @@ class CpuReference:
                 "fast_condition_aware": float(df.max() / np.abs(ref).max()),
                 "fast_strict_max_rel": float((df[nz] / np.abs(ref[nz])).max()),
                 "fast_frac_targets_above_1e-10": float((df[nz] / np.abs(ref[nz]) > 1e-10).mean())}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def cpu_baseline(system, cfg, econf, budget_pairs: float = 1.5e10):
@@ -327,7 +342,8 @@ def run_reference(args, cfg):
         log(f"reference step {i}: {res['sample']}")
     value = float(np.mean(vals))
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "particles/s",
+        "impl": "reference", "extrapolated": True, "metric": METRIC, "value": value,
+        "unit": "particles/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * cfg["n"] / value, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -335,7 +351,11 @@ def run_reference(args, cfg):
                    "degree": cfg["degree"], "leaf_size": econf.leaf_size,
                    "batch_size": econf.batch_size, "kernel": ["coulomb", "yukawa", "const"][cfg["kind"]]},
         "cpu_baseline": {"value": value, "unit": "particles/s", "cores": res["cores"],
-                         "kind": res["kind"], "sample": res["sample"]},
+                         "kind": res["kind"], "sample": res["sample"], "extrapolated": True,
+                         "cpu_model": res["cpu_model"],
+                         "sampled_pair_fraction": res["sampled_pair_fraction"],
+                         "anchor": "profiles/r2_cpu_full_step_*.json: unsampled full steps of "
+                                   "the same C port, checking the extrapolation"},
         "e2e": {"value": value, "unit": "particles/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -374,8 +394,7 @@ def run_ours(args, cfg):
     ctx = bltc.Context(local, stream.cuda_stream)
     mode = args.mode
     params = engine.make_params(econf, mode)
-    dfma = probe_fp64(local)
-    peak_tflops = 2.0 * dfma / 1e12
+    probe_tflops = 2.0 * probe_fp64(local) / 1e12
 
     if dist is not None:
         from paper_2003_01836_b200 import decomp
@@ -428,9 +447,8 @@ def run_ours(args, cfg):
     far_tflops = 2.0 * s_far * st.approx_pairs / far_s / 1e12 if far_s > 0 else 0.0
     near_tflops = 2.0 * s_near * st.direct_pairs / near_s / 1e12 if near_s > 0 else 0.0
     launches = l1 - l0   # every libbltc kernel launched in the timed region
-    # nominal FP64 peak: SMs x 64 FP64 lanes x 2 flop x max SM clock
+    # nominal FP64 peak: SMs x 64 FP64 lanes x 2 flop x the sampled SM clock
     sm_count = torch.cuda.get_device_properties(local).multi_processor_count
-    nominal_tflops = None
 
     # ---- e2e through the public API with host buffers (H2D/D2H inside)
     e2e = None
@@ -506,35 +524,43 @@ def run_ours(args, cfg):
                    "parallelism": f"rcb{world}" if world > 1 else "single",
                    "l2": "inputs (32 B/particle = 256 MB at 8M) larger than the 126 MB L2"},
         "phases_s": {"setup": st.setup_s, "precompute": st.precompute_s,
-                     "compute": st.compute_s, "far": far_s, "near": near_s},
+                     "compute": st.compute_s, "far": far_s, "near": near_s,
+                     "strict_certify_recompute": float(np.mean([x.strict_s for x in stats]))},
+        "strict": {"recomputed_targets": int(st.n_recomputed),
+                   "note": "STRICT: targets whose FAST value is not certified within 0.5e-10 "
+                           "of the reference are recomputed in the reference's arithmetic "
+                           "(-1: evaluated as PARITY)"},
         "pairs": {"approx": st.approx_pairs, "direct": st.direct_pairs,
                   "clusters": st.n_clusters, "batches": st.n_batches,
                   "moments": st.n_moments},
         "roofline": {"bound": "fp64",
                      "kernel": ("k_far_packed" if getattr(st, "packed", 0) else "k_far_fast") + " (far field)",
-                     "achieved": far_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
-                     "frac": far_tflops / peak_tflops if peak_tflops else None,
+                     "achieved": far_tflops, "peak": None, "unit": "TFLOP/s", "frac": None,
                      "traffic": traffic,
                      "work": f"{s_far} FP64 slots/pair x approx pairs (2 flop/slot)",
-                     "peak_source": "DFMA microbenchmark on this GPU in this run (bltc_probe_fp64, "
-                                    "sustained ~0.3 s)",
-                     "peak_nominal": nominal_tflops,
-                     "frac_nominal": far_tflops / nominal_tflops if nominal_tflops else None},
+                     "peak_source": "nominal FP64: SMs x 64 FP64 lanes x 2 flop x the median SM "
+                                    "clock sampled during the timed region (MEASURED_PEAKS.json "
+                                    "has no FP64 entry)",
+                     "peak_probe": probe_tflops,
+                     "peak_probe_source": "bltc_probe_fp64: sustained DFMA loop in this process "
+                                          "(~0.3 s), for reference"},
         "near_roofline": {"kernel": ("k_near_packed" if getattr(st, "packed", 0) else "k_near_fast")
-                                     + " (near field)", "achieved": near_tflops,
-                          "frac": near_tflops / peak_tflops if peak_tflops else None,
+                                     + " (near field)", "achieved": near_tflops, "frac": None,
                           "work": f"{s_near} FP64 slots/pair x direct pairs"},
-        "interaction_frac": ((2.0 * (s_far * st.approx_pairs + s_near * st.direct_pairs)
-                              / (far_s + near_s) / 1e12) / peak_tflops
-                             if far_s + near_s > 0 else None),
+        "interaction_tflops": (2.0 * (s_far * st.approx_pairs + s_near * st.direct_pairs)
+                               / (far_s + near_s) / 1e12) if far_s + near_s > 0 else None,
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
     csum = line["clocks"]
-    if csum.get("sm_max_mhz"):
-        nominal_tflops = sm_count * 64 * 2 * csum["sm_max_mhz"] * 1e6 / 1e12
-        line["roofline"]["peak_nominal"] = nominal_tflops
-        line["roofline"]["frac_nominal"] = far_tflops / nominal_tflops
+    f_mhz = csum.get("sm_mhz") or csum.get("sm_max_mhz")
+    if f_mhz:
+        nominal_tflops = sm_count * 64 * 2 * f_mhz * 1e6 / 1e12
+        line["roofline"]["peak"] = nominal_tflops
+        line["roofline"]["frac"] = far_tflops / nominal_tflops
+        line["near_roofline"]["frac"] = near_tflops / nominal_tflops
+        if line["interaction_tflops"]:
+            line["interaction_frac"] = line["interaction_tflops"] / nominal_tflops
     if e2e is not None:
         line["e2e"] = e2e
     cpu_ref = None
@@ -543,7 +569,8 @@ def run_ours(args, cfg):
             cpu_ref = CpuReference(system, econf, budget_pairs=args.ref_budget)
             cb = cpu_ref.step()
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind",
-                                                      "sample")}
+                                                      "sample", "extrapolated", "cpu_model",
+                                                      "sampled_pair_fraction")}
         except Exception as exc:   # the baseline is reported, never required
             line["cpu_baseline"] = {"value": None, "error": repr(exc)}
     if dist is None and not args.no_accuracy:
@@ -565,7 +592,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c4")
-    ap.add_argument("--mode", choices=["fast", "parity"], default="fast")
+    ap.add_argument("--mode", choices=["strict", "fast", "parity"], default="strict")
     ap.add_argument("--batch-size", type=int, default=None)
     ap.add_argument("--leaf-size", type=int, default=None)
     ap.add_argument("--ref-budget", type=float, default=1.5e10,

@@ -530,7 +530,7 @@ void build_batches(bltc_ctx* c, Partition& T) {
 // PARITY -- bitwise, so trivially within the tolerance.
 void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, const double* sx,
               const double* sy, const double* sz, const double* sq, const double4* src4,
-              const double* rows, int64_t n_rows, bltc_stats* stats) {
+              const double* rows, int64_t n_rows, int64_t n_src, bltc_stats* stats) {
   cudaStream_t st = c->st;
   const Partition& T = *c->tgt;
   EvalArgs a{};
@@ -628,7 +628,7 @@ void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, 
             BLTC_CUDA(cudaEventCreate(&e1));
             BLTC_CUDA(cudaEventRecord(e0, st));
           }
-          strict_fixup(a, p->kernel_code, n_rows, c->strict, T.n, st);
+          strict_fixup(a, p->kernel_code, n_rows, n_src, c->strict, T.n, st);
           c->n_recomputed = -2;   // on the device: read with the stats
           if (c->timing) {
             BLTC_CUDA(cudaEventRecord(e1, st));
@@ -765,7 +765,7 @@ void run_pipeline(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64
     BLTC_LAUNCH_CHECK();
   }
   evaluate(c, p, 1, c->ecl.p, c->src.x.p, c->src.y.p, c->src.z.p, c->src.q.p, c->src4.p,
-           c->rows.p, c->n_moments, stats);
+           c->rows.p, c->n_moments, n_s, stats);
   k_unpermute<<<grid_for(n_t, 256), 256, 0, st>>>(n_t, c->out_sorted.p, c->tgt->perm.p, phi_dev);
   BLTC_LAUNCH_CHECK();
   tr("evaluate");
@@ -1473,7 +1473,7 @@ int bltc_rank_evaluate(bltc_ctx* c, const bltc_params* p, int32_t ranks, int32_t
       BLTC_LAUNCH_CHECK();
     }
     evaluate(c, p, G, c->f_ecl.p, c->f_x.p, c->f_y.p, c->f_z.p, c->f_q.p, c->f_src4.p,
-             c->f_rows.p, RW, stats);
+             c->f_rows.p, RW, P, stats);
     const int64_t n = c->rank_n;
     c->phi_dev.resize(n);
     k_unpermute<<<grid_for(n, 256), 256, 0, st>>>(n, c->out_sorted.p, c->tgt->perm.p,
@@ -1729,7 +1729,7 @@ int bltc_stage_potentials(bltc_ctx* c, const bltc_params* p, const double* cheb_
       BLTC_LAUNCH_CHECK();
     }
     tm.mark();
-    evaluate(c, p, 1, c->ecl.p, S.x.p, S.y.p, S.z.p, S.q.p, c->src4.p, c->rows.p, n_rows,
+    evaluate(c, p, 1, c->ecl.p, S.x.p, S.y.p, S.z.p, S.q.p, c->src4.p, c->rows.p, n_rows, n_s,
              stats);
     c->phi_dev.resize(n_t);
     if (perm) {   // (out + carry)[perm] of compute_potentials (engine.py:335)

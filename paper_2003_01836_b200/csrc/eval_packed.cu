@@ -558,8 +558,18 @@ constexpr int kNearUnroll = BLTC_NEAR_UNROLL;   // pragma arguments are not macr
 // kFoldChunks chunks of 32 sources (C4 near 206.0 ms folding every chunk,
 // 204.3 every 2, 203.4 every 4, 202.7 every 8)
 constexpr int kFoldChunks = BLTC_FOLD_CHUNKS;
+// A non-negative double (2^-126 <= x < 2^128) as a float from its high
+// word alone, truncated to 20 mantissa bits (so <= x, within 2^-20):
+// integer-pipe work (IMNMX + LEA), no FP64 instruction.  Smaller x clamp up
+// to 2^-126 (an over-estimate; STRICT only needs an upper bound, and the
+// callers guard the range of |q|).
+__device__ __forceinline__ float hi_float(double x) {
+  const int h = max(__double2hiint(x), 0x38100000);
+  return __int_as_float((h - 0x38000000) << 3);
+}
+
 template <int KIND, int CH, bool MASKED, int FORM, bool ABS = false>
-__device__ __forceinline__ void near_chunk(double (&part)[2], double (&apart)[2],
+__device__ __forceinline__ void near_chunk(double (&part)[2], float (&apart)[2],
                                            const double4* src, const double (&tx)[2],
                                            const double (&ty)[2], const double (&tz)[2],
                                            const YukawaK& yk) {
@@ -567,17 +577,21 @@ __device__ __forceinline__ void near_chunk(double (&part)[2], double (&apart)[2]
 #pragma unroll kNearUnroll
   for (int j = 0; j < CH; ++j) {
     const double4 s = src[j];
+    // ABS: |q| f accumulated in FP32 on the integer / FP32 pipes (the FP64
+    // pipe is the near field's bound): the STRICT certificate's near mass
+    const float qa = ABS ? hi_float(fabs(s.w)) : 0.0f;
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       const double dx = __dsub_rn(tx[t], s.x);
       const double dy = __dsub_rn(ty[t], s.y);
       const double dz = __dsub_rn(tz[t], s.z);
       double d2, q;
+      bool ok = true;
       if (MASKED) {
         // d2 + 1e-300: exactly d2 for every non-singular pair, never 0, so
         // only the charge needs the select (excluded pairs add 0 * finite)
         d2 = fma(dz, dz, fma(dy, dy, fma(dx, dx, 1e-300)));
-        const bool ok = __double_as_longlong(d2) >= tb;
+        ok = __double_as_longlong(d2) >= tb;
         q = ok ? s.w : 0.0;
       } else {
         d2 = fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx)));
@@ -586,7 +600,7 @@ __device__ __forceinline__ void near_chunk(double (&part)[2], double (&apart)[2]
       if (ABS) {
         const double f = pair_factor<KIND>(d2, yk);
         part[t] = fma(q, f, part[t]);
-        apart[t] = fma(fabs(q), f, apart[t]);
+        apart[t] = fmaf(ok ? qa : 0.0f, hi_float(f), apart[t]);
       } else {
         part[t] = pair_acc<KIND, FORM>(part[t], q, d2, yk);
       }
@@ -825,7 +839,8 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
   }
   const double4* mine = wsm + L.g * NearSmem<CH>::kSeg;
   double npart[2] = {0.0, 0.0};   // FAST: partial sum over the last chunks
-  double apart[2] = {0.0, 0.0};   // ABS (STRICT): sum of |q f| over the pairs
+  float apart[2] = {0.0f, 0.0f};  // ABS (STRICT): sum of |q f| over the last chunks (FP32)
+  double aacc[2] = {0.0, 0.0};    // ABS: the folded FP32 partials
   int nchunk = 0;
   bool live = false;
 #pragma unroll
@@ -887,6 +902,10 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
           for (int t = 0; t < 2; ++t) {
             neumaier(acc[t], comp[t], npart[t]);
             npart[t] = 0.0;
+            if (ABS) {
+              aacc[t] += (double)apart[t];
+              apart[t] = 0.0f;
+            }
           }
         }
       }
@@ -913,9 +932,9 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
     if (L.v1) a.out[L.i1] = __dadd_rn(acc[1], comp[1]);
     return;
   }
-  if (ABS) {
-    if (L.v0) a.absum[L.i0] = apart[0];
-    if (L.v1) a.absum[L.i1] = apart[1];
+  if (ABS) {   // FP32 partials of <= 4 x 32 terms: relative rounding < 2^-16, covered
+    if (L.v0) a.absum[L.i0] = aacc[0] * (1.0 + 0x1p-12);
+    if (L.v1) a.absum[L.i1] = aacc[1] * (1.0 + 0x1p-12);
   }
   if (L.v0) {
     double total = acc[0], cmp = comp[0];

@@ -5,6 +5,7 @@
 #include "../paper_2003_01836_b200/csrc/eval_common.cuh"
 using namespace bltc;
 __device__ unsigned long long g_cnt[6];
+__device__ double g_bad[16];
 __global__ void k(long n, unsigned long long seed) {
   unsigned long long mism = 0, okc = 0, mism_d = 0, okd = 0, okr = 0, mism_r = 0;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
@@ -22,7 +23,14 @@ __global__ void k(long n, unsigned long long seed) {
     if (ok) { ++okd; if (__double_as_longlong(q) != __double_as_longlong(__ddiv_rn(a, s))) ++mism_d; }
     const double rb = (v - 0.5) * exp2(-1100.0 + 2200.0 * u);   // across the whole range
     const double r = rcp_rn_fastpath(rb, ok);
-    if (ok) { ++okr; if (__double_as_longlong(r) != __double_as_longlong(__drcp_rn(rb))) ++mism_r; }
+    if (ok) {
+      ++okr;
+      if (__double_as_longlong(r) != __double_as_longlong(__drcp_rn(rb))) {
+        ++mism_r;
+        const unsigned long long k = atomicAdd(&g_cnt[5], 0ull);
+        if (k < 16) g_bad[k] = rb;
+      }
+    }
   }
   atomicAdd(&g_cnt[4], okr); atomicAdd(&g_cnt[5], mism_r);
   atomicAdd(&g_cnt[0], okc); atomicAdd(&g_cnt[1], mism); atomicAdd(&g_cnt[2], okd); atomicAdd(&g_cnt[3], mism_d);
@@ -31,5 +39,7 @@ int main() {
   k<<<148 * 8, 256>>>(1L << 32, 777);
   unsigned long long h[6]; cudaMemcpyFromSymbol(h, g_cnt, sizeof(h));
   printf("{\"sqrt_fastpath\": %llu, \"sqrt_mismatch\": %llu, \"div_fastpath\": %llu, \"div_mismatch\": %llu, \"rcp_fastpath\": %llu, \"rcp_mismatch\": %llu}\n", h[0], h[1], h[2], h[3], h[4], h[5]);
+  double bad[16]; cudaMemcpyFromSymbol(bad, g_bad, sizeof(bad));
+  for (int i = 0; i < 16; ++i) printf("rcp mismatch operand %a\n", bad[i]);
   return 0;
 }
