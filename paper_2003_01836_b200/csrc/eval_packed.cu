@@ -560,26 +560,34 @@ constexpr int kNearUnroll = BLTC_NEAR_UNROLL;   // pragma arguments are not macr
 constexpr int kFoldChunks = BLTC_FOLD_CHUNKS;
 // A non-negative double (2^-126 <= x < 2^128) as a float from its high
 // word alone, truncated to 20 mantissa bits (so <= x, within 2^-20):
-// integer-pipe work (IMNMX + LEA), no FP64 instruction.  Smaller x clamp up
-// to 2^-126 (an over-estimate; STRICT only needs an upper bound, and the
-// callers guard the range of |q|).
+// integer-pipe work (LEA), no FP64 instruction.  CLAMP: smaller x clamp up
+// to 2^-126 (an over-estimate).
+template <bool CLAMP>
 __device__ __forceinline__ float hi_float(double x) {
-  const int h = max(__double2hiint(x), 0x38100000);
+  int h = __double2hiint(x);
+  if (CLAMP) h = max(h, 0x38100000);
   return __int_as_float((h - 0x38000000) << 3);
 }
 
-template <int KIND, int CH, bool MASKED, int FORM, bool ABS = false>
-__device__ __forceinline__ void near_chunk(double (&part)[2], float (&apart)[2],
-                                           const double4* src, const double (&tx)[2],
-                                           const double (&ty)[2], const double (&tz)[2],
-                                           const YukawaK& yk) {
+// STRICT's near-field mass sum_j |q_j| f_j (f = the kernel factor) per
+// target, variants (BLTC_ABS, measured in DESIGN.md 5.1):
+//   1: FP64, one more DFMA per pair (|q| f)
+//   2: FP32 on the integer / FP32 pipes: |q| from its high word (clamped),
+//      f from the rsqrt seed's high word (2^-20), one FFMA per pair
+//   3: FP32 sum of f from the seed's high word (one LEA + FADD per pair),
+//      times max |q| at the end
+// 2 and 3 need f in the float range: coordinates below 2^50 (guarded,
+// strict.cu) and zero-charge padding records at 2^60.
+template <int KIND, int CH, bool MASKED, int FORM, int ABS = 0>
+__device__ __forceinline__ void near_chunk(double (&part)[2], double (&apart)[2],
+                                           float (&fpart)[2], const double4* src,
+                                           const double (&tx)[2], const double (&ty)[2],
+                                           const double (&tz)[2], const YukawaK& yk) {
   const long long tb = __double_as_longlong(kSingularSq);   // d2 >= 0: bit order = value order
 #pragma unroll kNearUnroll
   for (int j = 0; j < CH; ++j) {
     const double4 s = src[j];
-    // ABS: |q| f accumulated in FP32 on the integer / FP32 pipes (the FP64
-    // pipe is the near field's bound): the STRICT certificate's near mass
-    const float qa = ABS ? hi_float(fabs(s.w)) : 0.0f;
+    const float qa = ABS == 2 ? hi_float<true>(fabs(s.w)) : 0.0f;
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       const double dx = __dsub_rn(tx[t], s.x);
@@ -597,10 +605,18 @@ __device__ __forceinline__ void near_chunk(double (&part)[2], float (&apart)[2],
         d2 = fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx)));
         q = s.w;
       }
-      if (ABS) {
+      if (ABS == 1) {
         const double f = pair_factor<KIND>(d2, yk);
         part[t] = fma(q, f, part[t]);
-        apart[t] = fmaf(ok ? qa : 0.0f, hi_float(f), apart[t]);
+        apart[t] = fma(fabs(q), f, apart[t]);
+      } else if (ABS >= 2) {
+        double y0;   // the rsqrt seed (2^-20): its high word is the mass estimate
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(d2));
+        // Yukawa: exp(-kappa r) / r <= 1 / r, the Coulomb mass bounds it
+        const float fa = hi_float<false>(y0);
+        if (ABS == 2) fpart[t] = fmaf(ok ? qa : 0.0f, fa, fpart[t]);
+        else fpart[t] += ok ? fa : 0.0f;
+        part[t] = pair_acc<KIND, 2>(part[t], q, d2, yk);
       } else {
         part[t] = pair_acc<KIND, FORM>(part[t], q, d2, yk);
       }
@@ -725,7 +741,7 @@ __device__ __forceinline__ bool stream_stage(const EvalArgs& a, const uint8_t* d
     cp_async16(dst + r0, sp);
     cp_async16(reinterpret_cast<char*>(dst + r0) + 16, reinterpret_cast<const char*>(sp) + 16);
   } else {
-    dst[r0] = make_double4(1e150, 1e150, 1e150, 0.0);   // contributes exactly 0
+    dst[r0] = make_double4(0x1p60, 0x1p60, 0x1p60, 0.0);   // contributes exactly 0
   }
   return need_mask;
 }
@@ -797,7 +813,7 @@ __device__ __forceinline__ bool near_stage_bulk(const EvalArgs& a, const uint8_t
       const int len = later ? __ffs(later) : 32 - lane;
       bulk_g2s(dst + lane, a.src4 + src[k], 32u * len, bar);
     } else if (!valid) {
-      dst[lane] = make_double4(1e150, 1e150, 1e150, 0.0);   // contributes exactly 0
+      dst[lane] = make_double4(0x1p60, 0x1p60, 0x1p60, 0.0);   // contributes exactly 0
     }
   }
   return __any_sync(0xffffffffu, need_mask);
@@ -807,7 +823,7 @@ __device__ __forceinline__ bool near_stage_bulk(const EvalArgs& a, const uint8_t
 // per-pair Neumaier compensation, out = acc + carry at the end (engine.py:
 // 302-312, 335); over several source groups one pass per group, (acc, carry)
 // handed from pass to pass (decomp.py:437-454).
-template <int KIND, int CH, int FORM, bool PAR = false, bool BULK = false, bool ABS = false>
+template <int KIND, int CH, int FORM, bool PAR = false, bool BULK = false, int ABS = 0>
 __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 it,
                                                  const int32_t* poff, const uint8_t* dmask,
                                                  double4* wsm, int lane, uint64_t* bar,
@@ -839,8 +855,9 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
   }
   const double4* mine = wsm + L.g * NearSmem<CH>::kSeg;
   double npart[2] = {0.0, 0.0};   // FAST: partial sum over the last chunks
-  float apart[2] = {0.0f, 0.0f};  // ABS (STRICT): sum of |q f| over the last chunks (FP32)
-  double aacc[2] = {0.0, 0.0};    // ABS: the folded FP32 partials
+  double apart[2] = {0.0, 0.0};   // ABS 1 (STRICT): sum of |q f| (FP64)
+  float fpart[2] = {0.0f, 0.0f};  // ABS 2 / 3: the last chunks' mass in FP32
+  double aacc[2] = {0.0, 0.0};    // ABS 2 / 3: the folded FP32 partials
   int nchunk = 0;
   bool live = false;
 #pragma unroll
@@ -893,18 +910,19 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
         }
       } else {
         if (masked)
-          near_chunk<KIND, CH, true, FORM, ABS>(npart, apart, mine + buf * CH, tx, ty, tz, a.yk);
+          near_chunk<KIND, CH, true, FORM, ABS>(npart, apart, fpart, mine + buf * CH, tx, ty,
+                                                tz, a.yk);
         else
-          near_chunk<KIND, CH, false, FORM, ABS>(npart, apart, mine + buf * CH, tx, ty, tz,
-                                                 a.yk);
+          near_chunk<KIND, CH, false, FORM, ABS>(npart, apart, fpart, mine + buf * CH, tx, ty,
+                                                 tz, a.yk);
         if ((++nchunk & (kFoldChunks - 1)) == 0 || !more) {   // fold every kFoldChunks chunks
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
             neumaier(acc[t], comp[t], npart[t]);
             npart[t] = 0.0;
-            if (ABS) {
-              aacc[t] += (double)apart[t];
-              apart[t] = 0.0f;
+            if (ABS >= 2) {
+              aacc[t] += (double)fpart[t];
+              fpart[t] = 0.0f;
             }
           }
         }
@@ -932,9 +950,13 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
     if (L.v1) a.out[L.i1] = __dadd_rn(acc[1], comp[1]);
     return;
   }
-  if (ABS) {   // FP32 partials of <= 4 x 32 terms: relative rounding < 2^-16, covered
-    if (L.v0) a.absum[L.i0] = aacc[0] * (1.0 + 0x1p-12);
-    if (L.v1) a.absum[L.i1] = aacc[1] * (1.0 + 0x1p-12);
+  if (ABS) {
+    // ABS 2 / 3: truncated high words (2^-19 per term) and FP32 partials of
+    // <= 4 x 32 positive terms (< 2^-16 relative): covered by 2^-12
+    // (ABS 3: strict.cu multiplies by max |q|)
+    const double sc = ABS == 1 ? 1.0 : 1.0 + 0x1p-12;
+    if (L.v0) a.absum[L.i0] = (ABS == 1 ? apart[0] : aacc[0]) * sc;
+    if (L.v1) a.absum[L.i1] = (ABS == 1 ? apart[1] : aacc[1]) * sc;
   }
   if (L.v0) {
     double total = acc[0], cmp = comp[0];
@@ -949,7 +971,7 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
 }
 
 template <int KIND, int CH, int MINB, int FORM, bool PAR = false, bool BULK = false,
-          bool ABS = false>
+          int ABS = 0>
 __global__ void __launch_bounds__(kWarps * 32, MINB)
 k_near_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int32_t* poff,
               const uint8_t* dmask, int* counter) {
@@ -1063,7 +1085,7 @@ bool far_packed_dispatch(const EvalArgs& a, const PackedItems& it, int* counter,
   }
 }
 
-template <int KIND, int CH = kNearCh, int FORM = 0, bool PAR = false, bool ABS = false>
+template <int KIND, int CH = kNearCh, int FORM = 0, bool PAR = false, int ABS = 0>
 void near_packed_launch(const EvalArgs& a, const PackedItems& it, int* counter,
                         cudaStream_t st) {
   const size_t smem = sizeof(double4) * kWarps * NearSmem<CH>::kWarp;
@@ -1240,8 +1262,16 @@ void launch_eval_packed(const EvalArgs& a, int kind, const PackedItems& it, int*
     if (kind == 0) near_packed_launch<0, kNearCh, 0, true>(a, it, counters + 1, st);
     else near_packed_launch<1, kNearCh, 0, true>(a, it, counters + 1, st);
   } else if (strict) {   // FORM 2 arithmetic plus the |term| sums
-    if (kind == 0) near_packed_launch<0, kNearCh, 2, false, true>(a, it, counters + 1, st);
-    else near_packed_launch<1, kNearCh, 2, false, true>(a, it, counters + 1, st);
+    const int v = tune_abs();
+    if (kind == 0) {
+      if (v == 1) near_packed_launch<0, kNearCh, 2, false, 1>(a, it, counters + 1, st);
+      else if (v == 2) near_packed_launch<0, kNearCh, 2, false, 2>(a, it, counters + 1, st);
+      else near_packed_launch<0, kNearCh, 2, false, 3>(a, it, counters + 1, st);
+    } else {
+      if (v == 1) near_packed_launch<1, kNearCh, 2, false, 1>(a, it, counters + 1, st);
+      else if (v == 2) near_packed_launch<1, kNearCh, 2, false, 2>(a, it, counters + 1, st);
+      else near_packed_launch<1, kNearCh, 2, false, 3>(a, it, counters + 1, st);
+    }
   } else if (tune_form() != 2) {
     if (kind == 0) near_packed_launch<0>(a, it, counters + 1, st);
     else near_packed_launch<1>(a, it, counters + 1, st);
@@ -1258,6 +1288,15 @@ void launch_eval_packed(const EvalArgs& a, int kind, const PackedItems& it, int*
     cudaEventDestroy(e1);
     cudaEventDestroy(e2);
   }
+}
+
+int tune_abs() {
+  // measured at C4 / C3 near field: FAST 203.4 / 33.2 ms; variant 1 224.5 /
+  // 35.5, 2 237.4 / 36.6, 3 224.3 / 35.2 (+14% recomputed targets): the
+  // kernel is close to issue-bound, so the FP32 variants' extra integer
+  // instructions cost more than one DFMA
+  const char* e = std::getenv("BLTC_ABS");
+  return e ? std::atoi(e) : 1;
 }
 
 }  // namespace bltc
