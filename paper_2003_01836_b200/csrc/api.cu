@@ -16,7 +16,8 @@
 namespace bltc {
 
 static thread_local std::string g_err;
-long long g_launch_count = 0;
+std::atomic<long long> g_launch_count{0};
+thread_local long long t_launch_count = 0;
 void set_error(const std::string& msg) { g_err = msg; }
 
 __global__ void k_moments(const double* sx, const double* sy, const double* sz,
@@ -409,13 +410,25 @@ void build_lists(bltc_ctx* c, const bltc_params* p, int G, const MacNode* const*
   }
   exclusive_scan_i32(L.a_cnt.p, L.a_ptr.p, nseg + 1, c->bs.scan_tmp, st);
   exclusive_scan_i32(L.d_cnt.p, L.d_ptr.p, nseg + 1, c->bs.scan_tmp, st);
+  // the CSR offsets are int32: check the entry totals in 64 bits first
+  L.tot64.resize(2);
+  sum_counts_i64(L.a_cnt.p, L.d_cnt.p, nseg, L.tot64.p, st);
   int32_t* h = (int32_t*)c->hs.get(64);
   BLTC_CUDA(cudaMemcpyAsync(h, L.a_ptr.p + nseg, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   BLTC_CUDA(cudaMemcpyAsync(h + 1, L.d_ptr.p + nseg, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   BLTC_CUDA(cudaMemcpyAsync(h + 2, c->flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  BLTC_CUDA(cudaMemcpyAsync(h + 4, L.tot64.p, 2 * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, st));
   BLTC_CUDA(cudaStreamSynchronize(st));
   if (h[2]) {
     set_error("interaction-list traversal stack overflow (tree too deep)");
+    throw UserError{BLTC_ERR_UNSUPPORTED};
+  }
+  const unsigned long long* t64 = reinterpret_cast<const unsigned long long*>(h + 4);
+  if (t64[0] > (unsigned long long)INT32_MAX - 1 || t64[1] > (unsigned long long)INT32_MAX - 1) {
+    set_error("interaction lists above 2^31 entries on one device (" + std::to_string(t64[0]) +
+              " approximation, " + std::to_string(t64[1]) +
+              " direct): split the targets across more ranks");
     throw UserError{BLTC_ERR_UNSUPPORTED};
   }
   L.n_approx = h[0];
@@ -566,8 +579,13 @@ void evaluate(bltc_ctx* c, const bltc_params* p, int G, const EvalCluster* ecl, 
   a.par_first = a.par_last = 1;
   const bool strict = p->mode == BLTC_MODE_STRICT &&
                       packed_supported(p->kernel_code, p->degree);
+  // FAST degrees whose per-batch far kernel cannot hold a moment row in
+  // shared memory (degree >= 15 without packed kernels) evaluate as PARITY
+  const bool fast_ok = p->mode != BLTC_MODE_FAST ||
+                       packed_supported(p->kernel_code, p->degree) ||
+                       fast_far_fits(p->degree);
   const bool as_parity = p->mode == BLTC_MODE_PARITY ||
-                         (p->mode == BLTC_MODE_STRICT && !strict);
+                         (p->mode == BLTC_MODE_STRICT && !strict) || !fast_ok;
   c->n_recomputed = as_parity && p->mode == BLTC_MODE_STRICT ? -1 : 0;
   const bool parity_packed = as_parity &&
                              packed_supported(p->kernel_code, p->degree) &&
@@ -718,7 +736,7 @@ void run_pipeline(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64
   c->params = *p;
   c->have_run = false;
   c->lists_staged = false;
-  const long long launches0 = g_launch_count;
+  const long long launches0 = t_launch_count;
   Timer tm(c->timing, st);
   upload_nodes(c, p, cheb_s);
   tm.mark();  // 0
@@ -785,7 +803,7 @@ void run_pipeline(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64
     stats->compute_s = tm.secs(2, 3);
     stats->total_s = tm.secs(0, 3);
     stats->n_moments = c->n_moments;
-    stats->kernel_launches = g_launch_count - launches0;
+    stats->kernel_launches = t_launch_count - launches0;
     stats->tree_depth = c->src.depth;
     stats->batch_depth = c->tgt->depth;
     stats->n_recomputed = read_recomputed(c);
@@ -1412,7 +1430,7 @@ int bltc_rank_evaluate(bltc_ctx* c, const bltc_params* p, int32_t ranks, int32_t
     }
     if (stats) std::memset(stats, 0, sizeof(*stats));
     cudaStream_t st = c->st;
-    const long long launches0 = g_launch_count;
+    const long long launches0 = t_launch_count;
     Timer tm(c->timing, st);
     tm.mark();
     // owner order of _eval_rank (decomp.py:437-454): local first, then the
@@ -1496,7 +1514,7 @@ int bltc_rank_evaluate(bltc_ctx* c, const bltc_params* p, int32_t ranks, int32_t
       stats->compute_s = tm.secs(1, 2);
       stats->total_s = tm.secs(0, 2);
       stats->n_moments = c->n_moments;
-      stats->kernel_launches = g_launch_count - launches0;
+      stats->kernel_launches = t_launch_count - launches0;
       stats->tree_depth = c->src.depth;
       stats->batch_depth = c->tgt->depth;
       stats->n_recomputed = read_recomputed(c);
@@ -1636,13 +1654,31 @@ int bltc_stage_potentials(bltc_ctx* c, const bltc_params* p, const double* cheb_
     c->have_run = false;
     c->params = *p;
     cudaStream_t st = c->st;
-    const long long launches0 = g_launch_count;
+    const long long launches0 = t_launch_count;
     Timer tm(c->timing, st);
     upload_nodes(c, p, cheb_s);
     tm.mark();
     const int m = p->degree + 1;
     const int64_t m3 = (int64_t)m * m * m;
     const int mstride = moment_stride(p->degree);
+    // batches must tile valid target ranges, the CSR offsets be monotone and
+    // perm index the targets (bad caller structures must not reach the device)
+    for (int64_t b = 0; b < n_batches; ++b) {
+      if (batch_start[b] < 0 || batch_stop[b] > n_t || batch_start[b] > batch_stop[b]) {
+        set_error("batch target range out of bounds");
+        throw UserError{BLTC_ERR_VALUE};
+      }
+      if (a_ptr[b] < 0 || a_ptr[b + 1] < a_ptr[b] || d_ptr[b] < 0 || d_ptr[b + 1] < d_ptr[b]) {
+        set_error("list offsets (a_ptr / d_ptr) must be non-negative and non-decreasing");
+        throw UserError{BLTC_ERR_VALUE};
+      }
+    }
+    if (perm)
+      for (int64_t i = 0; i < n_t; ++i)
+        if (perm[i] < 0 || perm[i] >= n_t) {
+          set_error("perm entry out of range");
+          throw UserError{BLTC_ERR_VALUE};
+        }
     // targets (batch order) and batches
     Partition& T = c->tgt_own;
     h2d(T.x, tx, n_t, st);
@@ -1753,7 +1789,7 @@ int bltc_stage_potentials(bltc_ctx* c, const bltc_params* p, const double* cheb_
       stats->compute_s = tm.secs(1, 2);
       stats->total_s = tm.secs(0, 2);
       stats->n_moments = n_rows;
-      stats->kernel_launches = g_launch_count - launches0;
+      stats->kernel_launches = t_launch_count - launches0;
       stats->n_recomputed = read_recomputed(c);
     }
   });

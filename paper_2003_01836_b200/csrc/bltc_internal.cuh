@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -56,12 +57,16 @@ void set_error(const std::string& msg);
   } while (0)
 
 // Every kernel launch is followed by exactly one BLTC_LAUNCH_CHECK(): it
-// checks the launch and counts it (bltc_stats.kernel_launches).
-extern long long g_launch_count;
-#define BLTC_LAUNCH_CHECK()              \
-  do {                                   \
-    BLTC_CUDA(cudaGetLastError());       \
-    ++::bltc::g_launch_count;            \
+// checks the launch and counts it -- process-wide (atomic: rank threads of
+// bltc_run_distributed launch concurrently; bltc_launch_count) and per host
+// thread (bltc_stats.kernel_launches of that thread's calls).
+extern std::atomic<long long> g_launch_count;
+extern thread_local long long t_launch_count;
+#define BLTC_LAUNCH_CHECK()                                          \
+  do {                                                               \
+    BLTC_CUDA(cudaGetLastError());                                   \
+    ::bltc::g_launch_count.fetch_add(1, std::memory_order_relaxed); \
+    ++::bltc::t_launch_count;                                        \
   } while (0)
 
 struct CudaFailure {};
@@ -187,6 +192,7 @@ struct Lists {
   DBuf<int32_t> a_cnt, d_cnt;   // scratch counts
   int64_t n_approx = 0, n_direct = 0;
   DBuf<unsigned long long> pairs;  // [2]: direct, approx
+  DBuf<unsigned long long> tot64;  // [2]: list entries (approx, direct) in 64 bits
 };
 
 // ---------------------------------------------------------------------------
@@ -195,5 +201,9 @@ void exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, DBuf<int32_t
                         cudaStream_t st);
 
 int ceil_div(int64_t a, int64_t b);
+// 64-bit sums of two int32 count arrays of n entries (into out[0], out[1],
+// zeroed here): the overflow check of the int32 CSR offsets
+void sum_counts_i64(const int32_t* a, const int32_t* b, int64_t n, unsigned long long* out,
+                    cudaStream_t st);
 
 }  // namespace bltc

@@ -512,4 +512,16 @@ void launch_eval_fast(const EvalArgs& a, int kind, const FastItems& far_items,
   }
 }
 
+// Whether the per-batch FAST far kernel's shared-memory slab (a whole
+// moment row per warp) fits the device's opt-in limit: up to degree 14.
+bool fast_far_fits(int degree) {
+  const int m = degree + 1;
+  const int m3 = m * m * m;
+  const size_t smem = sizeof(double) * kWarps * (3 * kMaxM + 1 + (size_t)((m3 + 1) & ~1));
+  int dev = 0, limit = 0;
+  BLTC_CUDA(cudaGetDevice(&dev));
+  BLTC_CUDA(cudaDeviceGetAttribute(&limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  return smem <= (size_t)limit;
+}
+
 }  // namespace bltc

@@ -71,7 +71,7 @@ extern "C" BLTC_API int bltc_probe_fp64(int device, double seconds, double* dfma
 
 extern "C" BLTC_API int bltc_launch_count(int64_t* out) {
   if (!out) return BLTC_ERR_VALUE;
-  *out = (int64_t)bltc::g_launch_count;
+  *out = (int64_t)bltc::g_launch_count.load();
   return BLTC_OK;
 }
 

@@ -1,6 +1,8 @@
 // Device-wide exclusive prefix sum (int32), used for CSR construction and
 // stream compaction.  Three-phase: per-block totals -> scan of totals
 // (recursive) -> per-block scan plus carried offset.
+#include <algorithm>
+
 #include "bltc_internal.cuh"
 
 namespace bltc {
@@ -106,6 +108,36 @@ void exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, DBuf<int32_t
     tmp.reserve(need);
   }
   scan_rec(in, out, n, tmp.p, st);
+}
+
+namespace {
+__global__ void k_sum_i64(const int32_t* __restrict__ a, const int32_t* __restrict__ b,
+                          int64_t n, unsigned long long* out) {
+  unsigned long long sa = 0, sb = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    sa += (unsigned long long)(unsigned)a[i];
+    sb += (unsigned long long)(unsigned)b[i];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    sb += __shfl_xor_sync(0xffffffffu, sb, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out, sa);
+    atomicAdd(out + 1, sb);
+  }
+}
+}  // namespace
+
+void sum_counts_i64(const int32_t* a, const int32_t* b, int64_t n, unsigned long long* out,
+                    cudaStream_t st) {
+  BLTC_CUDA(cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), st));
+  if (n <= 0) return;
+  int grid = (int)std::min<int64_t>((n + 255) / 256, 1184);
+  k_sum_i64<<<grid, 256, 0, st>>>(a, b, n, out);
+  BLTC_LAUNCH_CHECK();
 }
 
 }  // namespace bltc

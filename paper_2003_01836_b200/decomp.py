@@ -139,7 +139,11 @@ class DeviceRcb:
     is a stable device sort instead of numpy's argpartition, so the order of
     particles WITHIN a rank differs from the reference's (tree shapes and
     cluster memberships do not; only summation order in FAST sums does).
-    ``order`` stays on the device."""
+    ``order`` stays on the device.  When particles share the coordinate at a
+    cut's order statistic, the stable sort and numpy's introselect may put
+    different tied particles on the left: ``tied`` is then True and callers
+    fall back to the host rcb_partition (so each rank still gets exactly the
+    reference's particle set)."""
 
     def __init__(self, x, y, z, ranks: int):
         import torch
@@ -152,6 +156,7 @@ class DeviceRcb:
         lo = np.array([float(c.min().item()) for c in coords])
         hi = np.array([float(c.max().item()) for c in coords])
         self.order = torch.arange(n, device=x.device)
+        self.tied = False
         shares = np.array([(n * (r + 1)) // ranks - (n * r) // ranks for r in range(ranks)],
                           dtype=np.int64)
         self.rank_start = np.concatenate(([0], np.cumsum(shares)))
@@ -168,6 +173,8 @@ class DeviceRcb:
             self.order[start:stop] = idx[perm]
             sv = vals[perm]
             left_max, right_min = (float(v) for v in sv[[n_left - 1, n_left]].tolist())
+            if left_max == right_min:
+                self.tied = True
             cut = 0.5 * (left_max + right_min)
             lo_hi = hi.copy()
             lo_hi[axis] = cut
@@ -734,6 +741,9 @@ def run_distributed(system, config, ranks: int, threads: int = 1, mode: str | No
         x, y, z, q = (torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(dev)
                       for v in (x, y, z, q))
         part = DeviceRcb(x, y, z, ranks)
+        if part.tied:   # ties at a cut: the reference's own partition
+            x, y, z, q = (np.asarray(v) for v in (src.x, src.y, src.z, system.charges))
+            part = rcb_partition(system.sources, ranks)
     else:
         part = rcb_partition(system.sources, ranks)
     timings = {}

@@ -199,13 +199,36 @@ def compute_moments(tree, config, cluster_ids=None, mode=None, context=None) -> 
     return rows
 
 
+@dataclass(eq=False)
+class ClusterMoments:
+    """moments.py:40-43: one cluster's modified charges, k1-major."""
+
+    cluster_index: int
+    q_hat: np.ndarray
+
+
+def compute_all_moments(tree, config, mode=None, context=None) -> list:
+    """compute_all_moments (moments.py:147-150) on the device: a list indexed
+    by cluster, ClusterMoments for every eligible cluster (all extents
+    >= 1e-14, tree.py:205-206), None otherwise."""
+    t = flat_tree(tree)
+    ext = _f64(t.hi) - _f64(t.lo)
+    ids = np.nonzero(np.all(ext >= 1e-14, axis=1))[0]
+    rows = compute_moments(tree, config, ids, mode=mode, context=context)
+    out = [None] * len(t.start)
+    for k, ci in enumerate(ids):
+        out[int(ci)] = ClusterMoments(int(ci), rows[k])
+    return out
+
+
 def compute_potentials(batch_set, tree, moments, lists, config, threads: int = 1,
-                       mode=None, moment_row=None, context=None):
+                       mode=None, moment_row=None, context=None, return_stats: bool = False):
     """engine.py:315-335 on the device: all approximations then all direct
     sums per batch; phi in the original target order when the batches carry
     ``perm`` (batch order otherwise).  ``moments``: the reference's list of
     ClusterMoments-or-None indexed by cluster, or rows [n_rows][(n+1)^3] with
-    ``moment_row`` (cluster -> row, -1 for none).  Returns (phi, RunStats)."""
+    ``moment_row`` (cluster -> row, -1 for none).  Returns phi, like the
+    reference; (phi, RunStats) with ``return_stats``."""
     del threads
     ctx = context or default_context()
     b, t, L = flat_batches(batch_set), flat_tree(tree), flat_lists(lists)
@@ -234,4 +257,4 @@ def compute_potentials(batch_set, tree, moments, lists, config, threads: int = 1
         _f(_f64(t.hi)), _l(L.a_ptr), _l(L.a_idx) if len(L.a_idx) else None, _l(L.d_ptr),
         _l(L.d_idx) if len(L.d_idx) else None, _l(mrow), rows.shape[0],
         _f(rows) if rows.shape[0] else None, _l(b.perm), _f(phi), ctypes.byref(st)))
-    return phi, RunStats.from_c(st)
+    return (phi, RunStats.from_c(st)) if return_stats else phi

@@ -197,3 +197,24 @@ def test_single_process_let_matches_reference_fetch():
     for me in range(4):
         v = let_violations(forests[me], engines[me].needs(4, me, recs), me)
         assert v == {"sufficiency": 0, "minimality": 0}
+
+
+def test_device_rcb_flags_ties_at_a_cut():
+    """DeviceRcb (torch, here on CPU tensors) takes the reference's cuts with
+    stable sorts; when particles share the coordinate at a cut's order
+    statistic it flags ``tied`` (run_distributed then uses the reference's
+    own rcb_partition), and on continuous data it reproduces the reference's
+    rank SETS exactly."""
+    import torch
+    from paper_2003_01836_b200.decomp import DeviceRcb
+    g = np.arange(9, dtype=np.float64)   # 729 points: the first cut (364) falls in a tie
+    lattice = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3)
+    d = DeviceRcb(*(torch.from_numpy(np.ascontiguousarray(lattice[:, k])) for k in range(3)), 4)
+    assert d.tied
+    s = cli.generate_particles(5000, 3).sources
+    d = DeviceRcb(*(torch.from_numpy(np.asarray(v)) for v in (s.x, s.y, s.z)), 4)
+    assert not d.tied
+    ref = rcb_partition(s, 4)
+    for r in range(4):
+        mine = np.sort(d.rank_indices(r).numpy())
+        np.testing.assert_array_equal(mine, np.sort(np.asarray(ref.rank_indices(r))))

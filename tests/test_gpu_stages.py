@@ -84,11 +84,11 @@ def test_stage_potentials(bltc, case):
     rows = g["moments"][has]
     cfg = _cfg(bltc, g)
     phi, st = stages.compute_potentials(batches, tree, rows, lists, cfg, mode="parity",
-                                        moment_row=mrow)
+                                        moment_row=mrow, return_stats=True)
     ref = g["phi"]
     np.testing.assert_array_equal(phi, ref)
     assert (st.direct_pairs, st.approx_pairs) == (int(g["direct_pairs"]), int(g["approx_pairs"]))
-    phi_f, _ = stages.compute_potentials(batches, tree, rows, lists, cfg, mode="fast",
+    phi_f = stages.compute_potentials(batches, tree, rows, lists, cfg, mode="fast",
                                          moment_row=mrow)
     assert np.abs(phi_f - ref).max() <= 1e-13 * np.abs(ref).max()
 
@@ -101,3 +101,48 @@ def test_stage_potentials_validates(bltc):
     with pytest.raises(ValueError):
         stages.compute_potentials(batches, tree, np.zeros((0, 125)), lists, _cfg(bltc, g),
                                   moment_row=mrow)
+
+
+def test_stage_potentials_validates_batches_and_perm(bltc):
+    """Bad caller structures are rejected on the host (ValueError), before
+    any device read: batch ranges beyond the targets, non-monotone CSR
+    offsets, perm entries out of range."""
+    import copy
+    from paper_2003_01836_b200 import stages
+    g = golden("c1_coulomb")
+    tree, batches, lists = _structures(g)
+    has = g["moments_has"].astype(bool)
+    mrow = np.where(has, np.cumsum(has) - 1, -1)
+    rows = g["moments"][has]
+    cfg = _cfg(bltc, g)
+    bad = copy.copy(batches)
+    bad.stop = batches.stop.copy()
+    bad.stop[-1] = len(batches.x) + 5
+    with pytest.raises(ValueError, match="batch target range"):
+        stages.compute_potentials(bad, tree, rows, lists, cfg, mode="parity", moment_row=mrow)
+    bad = copy.copy(batches)
+    bad.perm = batches.perm.copy()
+    bad.perm[0] = len(batches.x)
+    with pytest.raises(ValueError, match="perm"):
+        stages.compute_potentials(bad, tree, rows, lists, cfg, mode="parity", moment_row=mrow)
+    badl = copy.copy(lists)
+    badl.a_ptr = lists.a_ptr.copy()
+    badl.a_ptr[1] = badl.a_ptr[2] + 1
+    with pytest.raises(ValueError):
+        stages.compute_potentials(batches, tree, rows, badl, cfg, mode="parity", moment_row=mrow)
+
+
+def test_compute_all_moments_reference_shape(bltc):
+    """compute_all_moments (moments.py:147-150): list indexed by cluster,
+    ClusterMoments for eligible clusters, None otherwise -- bitwise rows."""
+    from paper_2003_01836_b200 import stages
+    g = golden("plummer")
+    tree, _, _ = _structures(g)
+    mm = stages.compute_all_moments(tree, _cfg(bltc, g), mode="parity")
+    has = g["moments_has"].astype(bool)
+    assert len(mm) == len(has)
+    for ci, m in enumerate(mm):
+        assert (m is not None) == bool(has[ci])
+        if m is not None:
+            assert m.cluster_index == ci
+            np.testing.assert_array_equal(m.q_hat, g["moments"][ci])
