@@ -21,8 +21,14 @@ Exchange (``exchange=``):
   all-to-all of exactly those moment rows and particle slices.  Nothing else
   moves, so the fetch statistics are the reference's (``let_violations``
   counts stay zero) and the evaluation sees the same data as the reference.
-* ``"replicate"`` -- one all-gather of the whole forest (every rank holds a
-  superset of its LET; cheaper to orchestrate on one NVSwitch box).
+* ``"replicate"`` -- north_star's exchange and the default of the
+  one-process-per-GPU runner (``DeviceRankRunner``, bench.py N > 1): one
+  all-gather of three sizes per rank, then ONE all-gather of every rank's
+  packed [tree records | particles | moment rows] block, published by
+  libbltc straight into the send buffer (``publish_packed``).  Every rank
+  holds a superset of its LET; on one NVSwitch box moving the whole forest
+  (≈ 300 MB at 8M particles) costs well under a millisecond, less than the
+  LET's extra plan / serve round trips.
 
 Execution models:
 * ``torch.distributed`` initialised with world_size == ranks: this process is
@@ -206,6 +212,7 @@ class Published:
     records: object
     particles: object
     moments: object
+    block: object = None   # the packed [records | particles | moments] buffer, if any
 
     @property
     def sizes(self) -> tuple[int, int, int]:
@@ -256,37 +263,74 @@ def _all_reduce(t, group=None):
         dist.all_reduce(t, group=group)
 
 
-def all_gather_published(pub: Published, ranks: int, group=None) -> list[Published]:
-    """Replicate every rank's published data on every rank: one size
-    all-gather, then one padded all-gather per buffer (NCCL over NVLink for
-    CUDA tensors, gloo for CPU tensors)."""
+def packed_doubles(sizes, ncols: int) -> int:
+    """Doubles of one rank's packed publication [records | particles |
+    moment rows], rounded up to 32 (256-byte blocks, so every rank's block
+    and its moment rows stay aligned inside the gathered buffer)."""
+    nc, n, nrow = sizes
+    return (nc * RECORD_DOUBLES + 4 * n + nrow * ncols + 31) // 32 * 32
+
+
+def unpack_published(block, sizes, ncols: int) -> Published:
+    """Views of one rank's packed block (layout of ``packed_doubles``)."""
+    nc, n, nrow = sizes
+    o1 = nc * RECORD_DOUBLES
+    o2 = o1 + 4 * n
+    return Published(block[:o1].view(nc, RECORD_DOUBLES), block[o1:o2].view(4, n),
+                     block[o2:o2 + nrow * ncols].view(nrow, ncols))
+
+
+def _all_gather_flat(out, buf, ranks: int, group=None):
+    """out[ranks * buf.numel()] <- every rank's buf: NCCL's all_gather_into_
+    tensor (one collective, no per-rank output list) for CUDA tensors on an
+    NCCL group; the list form (host copies for gloo) otherwise."""
+    import torch.distributed as dist
+    if buf.is_cuda and dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, buf, group=group)
+    else:
+        _all_gather(list(out.view(ranks, -1).unbind(0)), buf, group=group)
+
+
+def all_gather_sizes(sizes, ranks: int, group=None, device=None) -> list[tuple]:
+    """Every rank's (n_clusters, n_particles, n_moment_rows): one tiny
+    all-gather, the step's only host read-back of the exchange."""
+    import torch
+    t = torch.tensor(sizes, dtype=torch.int64, device=device)
+    out = torch.empty(ranks * 3, dtype=torch.int64, device=device)
+    _all_gather_flat(out, t, ranks, group)
+    h = out.view(ranks, 3).tolist()
+    return [tuple(int(v) for v in s) for s in h]
+
+
+def all_gather_published(pub: Published, ranks: int, group=None,
+                         all_sizes: list | None = None) -> list[Published]:
+    """Replicate every rank's published data on every rank -- north_star's
+    single all-gather of the source tree, proxy charges and near-field
+    particles: one packed [records | particles | moments] block per rank,
+    padded to the largest rank's block, moved by ONE all-gather (NCCL over
+    NVLink for CUDA tensors, gloo for CPU tensors).  ``pub`` may already be a
+    view of a packed block (DeviceRankEngine.publish_packed); the sizes
+    all-gather is skipped when ``all_sizes`` is given."""
     import torch
 
     dev = pub.records.device
-    sizes = torch.tensor(pub.sizes, dtype=torch.int64, device=dev)
-    all_sizes = [torch.empty_like(sizes) for _ in range(ranks)]
-    _all_gather(all_sizes, sizes, group=group)
-    all_sizes = [tuple(int(v) for v in s.tolist()) for s in all_sizes]
-    ncols = pub.moments.shape[1]
-    out = []
-    flat = {}
-    for key, width, pos in (("records", RECORD_DOUBLES, 0), ("particles", 4, 1),
-                            ("moments", ncols, 2)):
-        counts = [s[pos] for s in all_sizes]
-        cap = max(1, max(counts)) * width
+    ncols = int(pub.moments.shape[1])
+    if all_sizes is None:
+        all_sizes = all_gather_sizes(pub.sizes, ranks, group, dev)
+    cap = max(packed_doubles(s, ncols) for s in all_sizes)
+    mine = getattr(pub, "block", None)
+    if mine is None or mine.numel() != cap:
         buf = torch.zeros(cap, dtype=torch.float64, device=dev)
-        mine = getattr(pub, key).reshape(-1)
-        buf[:mine.numel()] = mine
-        gathered = [torch.empty_like(buf) for _ in range(ranks)]
-        _all_gather(gathered, buf, group=group)
-        flat[key] = (gathered, counts)
-    for r in range(ranks):
-        nc, n, nrow = all_sizes[r]
-        rec = flat["records"][0][r][:nc * RECORD_DOUBLES].view(nc, RECORD_DOUBLES)
-        par = flat["particles"][0][r][:4 * n].view(4, n)
-        mom = flat["moments"][0][r][:nrow * ncols].view(nrow, ncols)
-        out.append(Published(rec, par, mom))
-    return out
+        nc, n, nrow = pub.sizes
+        o1, o2 = nc * RECORD_DOUBLES, nc * RECORD_DOUBLES + 4 * n
+        buf[:o1] = pub.records.reshape(-1)
+        buf[o1:o2] = pub.particles.reshape(-1)
+        buf[o2:o2 + nrow * ncols] = pub.moments.reshape(-1)
+        mine = buf
+    out = torch.empty(ranks * cap, dtype=torch.float64, device=dev)
+    _all_gather_flat(out, mine, ranks, group)
+    blocks = out.view(ranks, cap)
+    return [unpack_published(blocks[r], all_sizes[r], ncols) for r in range(ranks)]
 
 
 def all_gather_records(pub: Published, ranks: int, group=None) -> list:
@@ -606,13 +650,46 @@ class DeviceRankEngine:
                           dtype=torch.float64, device=dev)
         self._sync()
         self.ctx.rank_publish(rec.data_ptr(), par.data_ptr(), mom.data_ptr())
-        torch.cuda.synchronize(dev)
+        self._sync_after()
         return Published(rec, par, mom[:sz["n_moment_rows"]])
+
+    def publish_sizes(self) -> tuple:
+        sz = self.ctx.rank_publish_sizes()
+        return (int(sz["n_clusters"]), int(sz["n_particles"]), int(sz["n_moment_rows"]))
+
+    def publish_packed(self, cap: int) -> Published:
+        """Publish straight into one packed block of ``cap`` doubles
+        (decomp.packed_doubles layout), ready for all_gather_published's
+        single collective: no staging copies."""
+        torch = self.torch
+        sizes = self.publish_sizes()
+        ncols = moment_stride(self.params.degree)
+        block = torch.empty(cap, dtype=torch.float64, device=torch.device("cuda", self.device))
+        pub = unpack_published(block, sizes, ncols)
+        pub.block = block
+        self._sync()
+        # zero-row moment views still need a valid pointer (nothing is written)
+        mom_ptr = pub.moments.data_ptr() if sizes[2] else block.data_ptr()
+        self.ctx.rank_publish(pub.records.data_ptr(), pub.particles.data_ptr(), mom_ptr)
+        self._sync_after()
+        return pub
+
+    def _same_stream(self) -> bool:
+        cur = self.torch.cuda.current_stream(self.device).cuda_stream
+        return getattr(self.ctx, "stream", None) == cur
 
     def _sync(self):
         """Order torch's work before libbltc's when the context has its own
-        stream (a caller-supplied context)."""
-        self.torch.cuda.current_stream(self.device).synchronize()
+        stream (a caller-supplied context); nothing to do when libbltc runs
+        on torch's current stream (the rank contexts, the bench)."""
+        if not self._same_stream():
+            self.torch.cuda.current_stream(self.device).synchronize()
+
+    def _sync_after(self):
+        """Order libbltc's work before torch's (collectives on the published
+        buffers) when the context has its own stream."""
+        if not self._same_stream():
+            self.torch.cuda.synchronize(self.device)
 
     def needs(self, ranks: int, my_rank: int, records: list) -> list:
         """LET step one on the device: per owner, int32 need flags per cluster."""
@@ -830,7 +907,7 @@ class DeviceRankRunner:
     NCCL, evaluation of the local batches -- and returns the rank's stats."""
 
     def __init__(self, ctx, system, config, mode: str | None = None, group=None,
-                 exchange: str = "let"):
+                 exchange: str = "replicate"):
         import torch
         import torch.distributed as dist
         self.dist, self.group = dist, group
@@ -850,13 +927,19 @@ class DeviceRankRunner:
 
     def step(self):
         self.engine.build(*self.inputs)
-        pub = self.engine.publish()
         if self.exchange == "let":
+            pub = self.engine.publish()
             forest, self.fetch = let_exchange(
                 pub, lambda recs: self.engine.needs(self.ranks, self.me, recs), self.ranks,
                 self.me, self.group)
         else:
-            forest = all_gather_published(pub, self.ranks, self.group)
+            # north_star's exchange: one sizes all-gather (a few bytes), then
+            # ONE all-gather of every rank's packed tree / particles / moments
+            all_sizes = all_gather_sizes(self.engine.publish_sizes(), self.ranks, self.group,
+                                         self.inputs[0].device)
+            ncols = moment_stride(self.engine.params.degree)
+            pub = self.engine.publish_packed(max(packed_doubles(s, ncols) for s in all_sizes))
+            forest = all_gather_published(pub, self.ranks, self.group, all_sizes=all_sizes)
         self.phi = self.engine.evaluate(self.ranks, self.me, forest)
         return self.engine.stats
 

@@ -131,6 +131,7 @@ class Context:
         _lib.check(self._lib.bltc_create(int(device), ctypes.c_void_p(stream or 0),
                                          ctypes.byref(h)))
         self.handle = h
+        self.stream = stream or 0   # the CUDA stream handle libbltc runs on (0: its own)
 
     def close(self):
         if getattr(self, "handle", None):

@@ -218,3 +218,61 @@ def test_device_rcb_flags_ties_at_a_cut():
     for r in range(4):
         mine = np.sort(d.rank_indices(r).numpy())
         np.testing.assert_array_equal(mine, np.sort(np.asarray(ref.rank_indices(r))))
+
+
+def _packed_worker(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+
+    from paper_2003_01836_b200.decomp import (RECORD_DOUBLES, Published, all_gather_published,
+                                              all_gather_sizes, packed_doubles,
+                                              unpack_published)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ncols = 10
+
+    def make(r):   # ragged sizes, rank 1 without moment rows
+        nc, n, nrow = 3 + 2 * r, 5 + 7 * r, (0 if r == 1 else 2 + r)
+        g = torch.Generator().manual_seed(r)
+        return Published(torch.rand(nc, RECORD_DOUBLES, generator=g, dtype=torch.float64),
+                         torch.rand(4, n, generator=g, dtype=torch.float64),
+                         torch.rand(nrow, ncols, generator=g, dtype=torch.float64))
+
+    mine = make(rank)
+    # the staged path (pub given as three tensors) ...
+    forest = all_gather_published(mine, world)
+    # ... and the zero-copy path (pub already a view of a packed block)
+    sizes = all_gather_sizes(mine.sizes, world)
+    cap = max(packed_doubles(s, ncols) for s in sizes)
+    block = torch.zeros(cap, dtype=torch.float64)
+    view = unpack_published(block, mine.sizes, ncols)
+    view.records.copy_(mine.records)
+    view.particles.copy_(mine.particles)
+    view.moments.copy_(mine.moments)
+    view.block = block
+    forest2 = all_gather_published(view, world, all_sizes=sizes)
+    ok = True
+    for r in range(world):
+        want = make(r)
+        for f in (forest[r], forest2[r]):
+            ok &= f.sizes == want.sizes
+            ok &= bool(torch.equal(f.records, want.records) and
+                       torch.equal(f.particles, want.particles) and
+                       torch.equal(f.moments, want.moments))
+    np.save(os.path.join(out_dir, f"ok{rank}.npy"), np.array([ok]))
+    dist.destroy_process_group()
+
+
+def test_gloo_world3_packed_all_gather(tmp_path):
+    """The single packed all-gather of {records, particles, moment rows}
+    (north_star's one exchange): ragged per-rank sizes, a rank without
+    moment rows, staged and zero-copy publication -- every rank receives
+    every block exactly."""
+    import torch.multiprocessing as mp
+    mp.start_processes(_packed_worker, args=(3, _free_port(), str(tmp_path)), nprocs=3,
+                       join=True, start_method="spawn")
+    for r in range(3):
+        assert bool(np.load(tmp_path / f"ok{r}.npy")[0])

@@ -19,7 +19,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, case, out_dir):
+def _worker(rank, world, port, case, out_dir, backend="gloo"):
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
     sys.path.insert(0, here)
@@ -32,8 +32,13 @@ def _worker(rank, world, port, case, out_dir):
     from paper_2003_01836_b200.decomp import DeviceRankRunner, run_distributed
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(0)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = rank % torch.cuda.device_count() if backend == "nccl" else 0
+    torch.cuda.set_device(dev)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     g = golden(case)
     s = golden_system(g)
     kernel = [bltc.coulomb(), bltc.yukawa(float(g["kappa"]))][int(g["kind"])]
@@ -49,21 +54,34 @@ def _worker(rank, world, port, case, out_dir):
         np.save(os.path.join(out_dir, f"pairs_{exchange}{rank}.npy"),
                 np.array([st.direct_pairs, st.approx_pairs]))
     # the benchmark's per-rank runner (device-resident inputs), PARITY
-    ctx = bltc.Context(0)
-    runner = DeviceRankRunner(ctx, s, cfg, mode="parity")
-    runner.step()
-    np.save(os.path.join(out_dir, f"runner{rank}.npy"), runner.phi.cpu().numpy())
+    ctx = bltc.Context(dev, torch.cuda.current_stream(dev).cuda_stream)
+    for exchange in ("replicate", "let"):
+        runner = DeviceRankRunner(ctx, s, cfg, mode="parity", exchange=exchange)
+        runner.step()
+        runner.step()   # reused buffers / context
+        np.save(os.path.join(out_dir, f"runner_{exchange}{rank}.npy"), runner.phi.cpu().numpy())
     ctx.close()
     dist.destroy_process_group()
 
 
+def _n_gpus():
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.parametrize("backend", ["gloo", "nccl"])
 @pytest.mark.parametrize("case", ["dist_r3", "dist_r4_yukawa"])
-def test_process_group_ranks_match_reference(tmp_path, case):
+def test_process_group_ranks_match_reference(tmp_path, case, backend):
+    """gloo: every rank on the one GPU; nccl: one rank per GPU over NVLink
+    (the bench's N > 1 path: the single packed all-gather, and the LET) --
+    needs as many GPUs as ranks."""
     import torch.multiprocessing as mp
     from paper_2003_01836_b200.decomp import rcb_partition
     g = golden(case)
     R = int(g["ranks"])
-    mp.start_processes(_worker, args=(R, _free_port(), case, str(tmp_path)), nprocs=R,
+    if backend == "nccl" and _n_gpus() < R:
+        pytest.skip(f"NCCL ranks need {R} GPUs, {_n_gpus()} visible")
+    mp.start_processes(_worker, args=(R, _free_port(), case, str(tmp_path), backend), nprocs=R,
                        join=True, start_method="spawn")
     part = rcb_partition(golden_system(g).sources, R)
     for r in range(R):
@@ -76,6 +94,7 @@ def test_process_group_ranks_match_reference(tmp_path, case):
         mine = np.load(tmp_path / f"fetch_let{r}.npy")
         np.testing.assert_array_equal(mine, g["fetch"][g["fetch"][:, 0] == r])
         # the runner's rank slice equals the assembled result on its targets
-        run = np.load(tmp_path / f"runner{r}.npy")
-        np.testing.assert_array_equal(run, np.load(tmp_path / f"phi_let{r}.npy")[
-            part.rank_indices(r)])
+        for ex in ("replicate", "let"):
+            run = np.load(tmp_path / f"runner_{ex}{r}.npy")
+            np.testing.assert_array_equal(run, np.load(tmp_path / f"phi_let{r}.npy")[
+                part.rank_indices(r)])
