@@ -280,7 +280,10 @@ struct bltc_ctx {
 
 namespace {
 
-void check_params(const bltc_params* p) {
+// Validates the parameters and returns them normalised: Yukawa with kappa = 0
+// is the Coulomb kernel (exp(-0 r) q / r == q / r bitwise in the reference,
+// engine.py:190-191; the FAST / STRICT paths then match Coulomb bitwise too).
+bltc_params check_params(const bltc_params* p) {
   if (!p) {
     set_error("params is NULL");
     throw UserError{BLTC_ERR_VALUE};
@@ -314,6 +317,9 @@ void check_params(const bltc_params* p) {
     set_error("mode must be BLTC_MODE_PARITY, BLTC_MODE_FAST or BLTC_MODE_STRICT");
     throw UserError{BLTC_ERR_VALUE};
   }
+  bltc_params n = *p;
+  if (n.kernel_code == 1 && n.kappa == 0.0) n.kernel_code = 0;
+  return n;
 }
 
 template <typename F>
@@ -723,7 +729,8 @@ void run_pipeline(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64
                   const double* sx, const double* sy, const double* sz, const double* q,
                   bool coincident, double* phi_dev, bltc_stats* stats,
                   bool evaluate_phi = true) {
-  check_params(p);
+  const bltc_params pn_ = check_params(p);
+  p = &pn_;
   if (n_s < 1 || n_t < 1) {
     set_error("cannot partition an empty particle set");
     throw UserError{BLTC_ERR_VALUE};
@@ -999,7 +1006,8 @@ int bltc_build(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64_t 
     if (!c) throw UserError{BLTC_ERR_VALUE};
     BLTC_CUDA(cudaSetDevice(c->device));
     if (stats) std::memset(stats, 0, sizeof(*stats));
-    check_params(p);
+    const bltc_params pn_ = check_params(p);
+    p = &pn_;
     if (n_s < 1 || n_t < 1) {
       set_error("cannot partition an empty particle set");
       throw UserError{BLTC_ERR_VALUE};
@@ -1037,7 +1045,8 @@ int bltc_treecode(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int64
     if (!c) throw UserError{BLTC_ERR_VALUE};
     BLTC_CUDA(cudaSetDevice(c->device));
     if (stats) std::memset(stats, 0, sizeof(*stats));
-    check_params(p);
+    const bltc_params pn_ = check_params(p);
+    p = &pn_;
     if (n_s < 1 || n_t < 1) {
       set_error("cannot partition an empty particle set");
       throw UserError{BLTC_ERR_VALUE};
@@ -1241,7 +1250,8 @@ int bltc_rank_build(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int
   return guarded([&] {
     if (!c) throw UserError{BLTC_ERR_VALUE};
     BLTC_CUDA(cudaSetDevice(c->device));
-    check_params(p);
+    const bltc_params pn_ = check_params(p);
+    p = &pn_;
     if (n < 1) {
       set_error("cannot partition an empty particle set");
       throw UserError{BLTC_ERR_VALUE};
@@ -1344,7 +1354,8 @@ int bltc_rank_needs(bltc_ctx* c, const bltc_params* p, int32_t ranks, int32_t my
       throw UserError{BLTC_ERR_STATE};
     }
     BLTC_CUDA(cudaSetDevice(c->device));
-    check_params(p);
+    const bltc_params pn_ = check_params(p);
+    p = &pn_;
     if (ranks < 1 || my_rank < 0 || my_rank >= ranks) {
       set_error("invalid ranks / my_rank");
       throw UserError{BLTC_ERR_VALUE};
@@ -1418,7 +1429,8 @@ int bltc_rank_evaluate(bltc_ctx* c, const bltc_params* p, int32_t ranks, int32_t
       throw UserError{BLTC_ERR_STATE};
     }
     BLTC_CUDA(cudaSetDevice(c->device));
-    check_params(p);
+    const bltc_params pn_ = check_params(p);
+    p = &pn_;
     if (ranks < 1 || my_rank < 0 || my_rank >= ranks) {
       set_error("invalid ranks / my_rank");
       throw UserError{BLTC_ERR_VALUE};
@@ -1536,7 +1548,8 @@ int bltc_stage_lists(bltc_ctx* c, const bltc_params* p, int64_t n_batches,
       set_error("ctx is NULL");
       throw UserError{BLTC_ERR_VALUE};
     }
-    check_params(p);
+    const bltc_params pn_ = check_params(p);
+    p = &pn_;
     BLTC_CUDA(cudaSetDevice(c->device));
     if (n_batches < 1 || n_clusters < 1) {
       set_error("need at least one batch and one cluster");
@@ -1572,7 +1585,8 @@ int bltc_stage_moments(bltc_ctx* c, const bltc_params* p, const double* cheb_s, 
       set_error("ctx is NULL");
       throw UserError{BLTC_ERR_VALUE};
     }
-    check_params(p);
+    const bltc_params pn_ = check_params(p);
+    p = &pn_;
     BLTC_CUDA(cudaSetDevice(c->device));
     if (n_s < 1 || n_clusters < 1) {
       set_error("need at least one source and one cluster");
@@ -1636,7 +1650,8 @@ int bltc_stage_potentials(bltc_ctx* c, const bltc_params* p, const double* cheb_
       set_error("ctx is NULL");
       throw UserError{BLTC_ERR_VALUE};
     }
-    check_params(p);
+    const bltc_params pn_ = check_params(p);
+    p = &pn_;
     BLTC_CUDA(cudaSetDevice(c->device));
     if (n_t < 1 || n_s < 1 || n_batches < 1 || n_clusters < 1) {
       set_error("need targets, sources, batches and clusters");

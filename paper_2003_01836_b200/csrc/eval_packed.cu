@@ -34,6 +34,7 @@
 
 #include "bltc_internal.cuh"
 #include "eval_common.cuh"
+#include "exp2w_table.h"
 
 #include <cstdio>
 #include <cstdlib>
@@ -268,28 +269,37 @@ __global__ void k_window_fill(int64_t nb, const int32_t* poff, int64_t nw, const
 // Per direct-list entry: can a pair of (batch, cluster) be singular?  The
 // singular-pair test (d^2 < 1e-28, engine.py:175) can only fire if the
 // batch ball comes within ~1e-14 of the cluster box.
+// Also, per batch (bys): can the Yukawa near field use the shifted-exp table
+// with s = 0 -- every pair of the batch's direct list within c r + 2 <= 2048
+// (r <= |batch center - cluster center| + batch radius + half diagonal)?
 __global__ void k_direct_mask(int64_t nb, int G, const int32_t* d_ptr, const int32_t* d_idx,
                               const EvalCluster* clusters, const double* bcenter,
-                              const double* bradius, uint8_t* mask) {
+                              const double* bradius, uint8_t* mask, double c2, uint8_t* bys) {
   const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (b >= nb) return;
   const double* bc = bcenter + 3 * b;
   const double br = bradius[b];
   const double scale = fmax(fmax(fabs(bc[0]), fabs(bc[1])), fabs(bc[2])) + br;
+  bool ys = true;
   for (int e = d_ptr[b * G]; e < d_ptr[(b + 1) * G]; ++e) {
     const EvalCluster& c = clusters[d_idx[e]];
-    double g2 = 0.0;
+    double g2 = 0.0, cd2 = 0.0, hd2 = 0.0;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       const double lo = c.lo[d] - bc[d], hi = bc[d] - c.hi[d];
       const double g = fmax(fmax(lo, hi), 0.0);
       g2 = fma(g, g, g2);
+      const double cc = 0.5 * (c.lo[d] + c.hi[d]) - bc[d], ex = 0.5 * (c.hi[d] - c.lo[d]);
+      cd2 = fma(cc, cc, cd2);
+      hd2 = fma(ex, ex, hd2);
     }
+    ys &= c2 * (sqrt(cd2) + br + sqrt(hd2)) * (1.0 + 1e-12) + 2.0 <= (double)kExp2WK;
     mask[e] = (sqrt(g2) - br) <= 1e-12 * (1.0 + scale) ? 1 : 0;
 #ifdef BLTC_DEBUG_NOMASK
     mask[e] = 0;   // timing experiment only: wrong results for singular pairs
 #endif
   }
+  bys[b] = ys ? 1 : 0;
 }
 
 // Lane layout of one item: slots slot_begin + 2 lane, +1.
@@ -363,9 +373,103 @@ __device__ __forceinline__ void far_stage_slab(double* wsm, const FarHdr* H, int
 // DY: dy^2 per (target, k2) computed once per cluster into lane-private
 // shared-memory slots, so a row costs one DADD per target (dx^2 + dy^2)
 // instead of a DSUB and a DFMA.
-template <int KIND, int M, int KU, int FORM, bool PAR = false, bool DY = false>
+// FAST Yukawa far field with a shifted exponential (YS): per (target,
+// cluster) s = rint(c r_ref), r_ref = |target - box center|, c = kappa 2048 /
+// ln2, so that for every proxy point exp(-kappa r) = 2^(-s/2048) 2^(w/2048),
+// w = s - c r, |w| <= c hd + 1 (hd: the box's half diagonal).  With S = magic
+// + s, z = RN(S - c r) is magic + k (k = rint(w): the low word), S - z = s - k
+// exactly and f = w - k = fma(r, -c, S - z): the table T[k] = 2^(k/2048)
+// (kExp2W, |k| <= 2048, staged in shared memory) times a degree-3 Taylor
+// polynomial of 2^(f/2048) (truncation 3.4e-17) -- no exponent assembly and
+// no clamp in the pair loop (16 FP64 slots per pair instead of 17, and ~5
+// fewer integer instructions); the 2^(-s/2048) factor is applied once per
+// (target, cluster).  Clusters with c hd + 2 > 2048, or targets with
+// c r_ref >= 2^49, take the generic exp_neg_kr path for that step.
+struct YsState {
+  double S;    // magic + s
+  double E;    // 2^(-s/2048)
+};
+
+__device__ __forceinline__ double ys_pair_factor(double d2, double c, double S,
+                                                 const double* __restrict__ T0) {
+  const double y = rsqrt_fast(d2);
+  const double r = __dmul_rn(d2, y);
+  const double z = fma(r, -c, S);
+  const int k = __double2loint(z);
+  const double f = fma(r, -c, __dsub_rn(S, z));
+  constexpr double a1 = 0x1.62e42fefa39efp-12;   // ln2 / 2048
+  constexpr double a2 = a1 * a1 / 2.0;
+  constexpr double a3 = a1 * a1 * a1 / 6.0;
+  double p = fma(a3, f, a2);
+  p = fma(p, f, a1);
+  p = fma(p, f, 1.0);
+  return __dmul_rn(__dmul_rn(T0[k], p), y);
+}
+
+// The near field's YS factor with s = 0: k = rint(-c r) <= 0; the index is
+// clamped into [-2048, 0] for the zero-charge padding records far away
+// (their factor is then finite garbage times q = 0).
+__device__ __forceinline__ double ys_pair_factor_near(double d2, double c,
+                                                      const double* __restrict__ T0) {
+  const double kMagic = 6755399441055744.0;   // 1.5 * 2^52
+  const double y = rsqrt_fast(d2);
+  const double r = __dmul_rn(d2, y);
+  const double z = fma(r, -c, kMagic);
+  const int k = -(int)umin((unsigned)(-__double2loint(z)), (unsigned)kExp2WK);   // [-2048, 0]
+  const double f = fma(r, -c, __dsub_rn(kMagic, z));
+  constexpr double a1 = 0x1.62e42fefa39efp-12;   // ln2 / 2048
+  constexpr double a2 = a1 * a1 / 2.0;
+  constexpr double a3 = a1 * a1 * a1 / 6.0;
+  double p = fma(a3, f, a2);
+  p = fma(p, f, a1);
+  p = fma(p, f, 1.0);
+  return __dmul_rn(__dmul_rn(T0[k], p), y);
+}
+
+__device__ __forceinline__ YsState ys_state(double tx, double ty, double tz, double cx, double cy,
+                                            double cz, double c, const double* __restrict__ T0,
+                                            bool& ok) {
+  const double kMagic = 6755399441055744.0;   // 1.5 * 2^52
+  const double dx = tx - cx, dy = ty - cy, dz = tz - cz;
+  const double u = c * sqrt(fma(dx, dx, fma(dy, dy, dz * dz)));
+  ok = u < 0x1p49;
+  const double sd = ok ? rint(u) : 0.0;
+  YsState st;
+  st.S = kMagic + sd;
+  // 2^(-s/2048) = 2^(-m) T[-j], s = 2048 m + j, 0 <= j < 2048
+  const long long si = (long long)sd;
+  const int j = (int)(si & 2047);
+  const long long m = si >> 11;
+  st.E = m > 1100 ? 0.0 : ldexp(T0[-j], -(int)m);
+  return st;
+}
+
+// One cluster's FAST Yukawa far-field sum for one target, generic exponential,
+// moments from global memory: the YS kernel's rare fallback, kept out of line
+// so the hot loop stays small.
+template <int M>
+__device__ __noinline__ double far_cluster_generic(const double* __restrict__ row,
+                                                   const double* __restrict__ pts, double tx,
+                                                   double ty, double tz, YukawaK yk) {
+  double part = 0.0;
+  for (int k1 = 0; k1 < M; ++k1) {
+    const double dx = tx - pts[k1];
+    for (int k2 = 0; k2 < M; ++k2) {
+      const double dy = ty - pts[M + k2];
+      const double dxy = fma(dy, dy, dx * dx);
+      for (int k3 = 0; k3 < M; ++k3) {
+        const double dz = tz - pts[2 * M + k3];
+        part = pair_acc<1, 2>(part, row[(k1 * M + k2) * M + k3], fma(dz, dz, dxy), yk);
+      }
+    }
+  }
+  return part;
+}
+
+template <int KIND, int M, int KU, int FORM, bool PAR = false, bool DY = false, bool YS = false>
 __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it,
-                                                const int32_t* poff, double* wsm, int lane) {
+                                                const int32_t* poff, double* wsm, int lane,
+                                                const double* __restrict__ T0 = nullptr) {
   using SM = FarSmem<M>;
   double* dys = wsm + SM::kWarp + lane;   // DY slots: dys[(k2 * 2 + t) * 32]
   FarHdr* H = reinterpret_cast<FarHdr*>(wsm);
@@ -427,6 +531,36 @@ __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it
     double part[2] = {0.0, 0.0};
     bool slow[2] = {false, false};   // PAR, Coulomb: an operand left the fast path
     __syncwarp();   // proxy points (plain stores) visible to the warp
+    YsState ys[2];
+    bool use_ys = false;
+    if constexpr (YS) {
+      // bounds from the lane's OWN segment's staged proxy points (current, or
+      // stale for an idle segment -- its results are discarded, but its table
+      // index must stay in range too): box [p[M-1], p[0]] per axis
+      const double ex = mpts[0] - mpts[M - 1], ey = mpts[M] - mpts[2 * M - 1],
+                   ez = mpts[2 * M] - mpts[3 * M - 1];
+      const double hd = 0.5 * sqrt(fma(ex, ex, fma(ey, ey, ez * ez)));
+      const double cx = 0.5 * (mpts[0] + mpts[M - 1]);
+      const double cy = 0.5 * (mpts[M] + mpts[2 * M - 1]);
+      const double cz = 0.5 * (mpts[2 * M] + mpts[3 * M - 1]);
+      bool ok0, ok1;
+      ys[0] = ys_state(tx[0], ty[0], tz[0], cx, cy, cz, a.yk.c2, T0, ok0);
+      ys[1] = ys_state(tx[1], ty[1], tz[1], cx, cy, cz, a.yk.c2, T0, ok1);
+      use_ys = __all_sync(0xffffffffu, ok0 && ok1 && a.yk.c2 * hd + 2.0 <= (double)kExp2WK);
+      if (!use_ys) {
+        // rare: a cluster too large for the table at this kappa -- the
+        // generic exponential, straight from the moment row in global memory
+        cp_async_wait<0>();
+        __syncwarp();
+        const double* row = H->row[L.g];
+#pragma unroll 1
+        for (int t = 0; t < 2; ++t)
+          part[t] = act ? far_cluster_generic<M>(row, mpts, tx[t], ty[t], tz[t], a.yk) : 0.0;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) acc[t] = act ? __dadd_rn(acc[t], part[t]) : acc[t];
+        continue;
+      }
+    }
     double dz2[2][M];
 #pragma unroll
     for (int k3 = 0; k3 < M; ++k3) {
@@ -488,6 +622,8 @@ __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it
               slow[t] |= !ok;
             } else if (PAR) {
               part[t] = __dadd_rn(part[t], parity_term<KIND>(qv, d2, a.kappa));
+            } else if (YS) {
+              part[t] = fma(qv, ys_pair_factor(d2, a.yk.c2, ys[t].S, T0), part[t]);
             } else {
               part[t] = pair_acc<KIND, FORM>(part[t], qv, d2, a.yk);
             }
@@ -520,6 +656,10 @@ __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it
         part[t] = p;
       }
     }
+    if (YS) {
+#pragma unroll
+      for (int t = 0; t < 2; ++t) part[t] = __dmul_rn(part[t], ys[t].E);
+    }
 #pragma unroll
     for (int t = 0; t < 2; ++t) acc[t] = act ? __dadd_rn(acc[t], part[t]) : acc[t];
   }
@@ -527,15 +667,26 @@ __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it
   if (L.v1) a.far_out[L.i1] = acc[1];
 }
 
-template <int KIND, int M, int MINB, int KU, int FORM, bool PAR = false, bool DY = false>
+template <int KIND, int M, int MINB, int KU, int FORM, bool PAR = false, bool DY = false,
+          bool YS = false>
 __global__ void __launch_bounds__(kWarps * 32, MINB)
 k_far_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int32_t* poff,
              int* counter) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* wsm = smem + warp * (FarSmem<M>::kWarp + (DY ? FarSmem<M>::kDy : 0));
+  constexpr int kPerWarp = FarSmem<M>::kWarp + (DY ? FarSmem<M>::kDy : 0);
+  double* wsm = smem + warp * kPerWarp;
+  const double* T0 = nullptr;
+  if constexpr (YS) {   // the shifted-exp table behind the warps' regions
+    double* tab = smem + kWarps * kPerWarp;
+    for (int i = threadIdx.x; i < 2 * kExp2WK + 1; i += blockDim.x) tab[i] = kExp2W[i];
+    // proxy points of never-used segments: a point box (bounded table index)
+    for (int i = threadIdx.x; i < kWarps * kPerWarp; i += blockDim.x) smem[i] = 0.0;
+    __syncthreads();
+    T0 = tab + kExp2WK;
+  }
   for (int item = next_item(counter); item < n_items; item = next_item(counter))
-    far_packed_item<KIND, M, KU, FORM, PAR, DY>(a, items[item], poff, wsm, lane);
+    far_packed_item<KIND, M, KU, FORM, PAR, DY, YS>(a, items[item], poff, wsm, lane, T0);
 }
 
 // ---------------------------------------------------------------------------
@@ -578,11 +729,12 @@ __device__ __forceinline__ float hi_float(double x) {
 //      times max |q| at the end
 // 2 and 3 need f in the float range: coordinates below 2^50 (guarded,
 // strict.cu) and zero-charge padding records at 2^60.
-template <int KIND, int CH, bool MASKED, int FORM, int ABS = 0>
+template <int KIND, int CH, bool MASKED, int FORM, int ABS = 0, bool YS = false>
 __device__ __forceinline__ void near_chunk(double (&part)[2], double (&apart)[2],
                                            float (&fpart)[2], const double4* src,
                                            const double (&tx)[2], const double (&ty)[2],
-                                           const double (&tz)[2], const YukawaK& yk) {
+                                           const double (&tz)[2], const YukawaK& yk,
+                                           const double* __restrict__ T0 = nullptr) {
   const long long tb = __double_as_longlong(kSingularSq);   // d2 >= 0: bit order = value order
 #pragma unroll kNearUnroll
   for (int j = 0; j < CH; ++j) {
@@ -605,7 +757,11 @@ __device__ __forceinline__ void near_chunk(double (&part)[2], double (&apart)[2]
         d2 = fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx)));
         q = s.w;
       }
-      if (ABS == 1) {
+      if (YS) {   // Yukawa, shifted-exp table with s = 0 (the batch's flag holds)
+        const double f = ys_pair_factor_near(d2, yk.c2, T0);
+        part[t] = fma(q, f, part[t]);
+        if (ABS == 1) apart[t] = fma(fabs(q), f, apart[t]);
+      } else if (ABS == 1) {
         const double f = pair_factor<KIND>(d2, yk);
         part[t] = fma(q, f, part[t]);
         apart[t] = fma(fabs(q), f, apart[t]);
@@ -823,11 +979,13 @@ __device__ __forceinline__ bool near_stage_bulk(const EvalArgs& a, const uint8_t
 // per-pair Neumaier compensation, out = acc + carry at the end (engine.py:
 // 302-312, 335); over several source groups one pass per group, (acc, carry)
 // handed from pass to pass (decomp.py:437-454).
-template <int KIND, int CH, int FORM, bool PAR = false, bool BULK = false, int ABS = 0>
+template <int KIND, int CH, int FORM, bool PAR = false, bool BULK = false, int ABS = 0,
+          bool YS = false>
 __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 it,
                                                  const int32_t* poff, const uint8_t* dmask,
                                                  double4* wsm, int lane, uint64_t* bar,
-                                                 unsigned& phase) {
+                                                 unsigned& phase,
+                                                 const double* __restrict__ T0 = nullptr) {
   const LaneTargets L = lane_targets(it, a, poff, lane);
   const double tx[2] = {a.tx[L.i0], a.tx[L.i1]};
   const double ty[2] = {a.ty[L.i0], a.ty[L.i1]};
@@ -910,11 +1068,11 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
         }
       } else {
         if (masked)
-          near_chunk<KIND, CH, true, FORM, ABS>(npart, apart, fpart, mine + buf * CH, tx, ty,
-                                                tz, a.yk);
+          near_chunk<KIND, CH, true, FORM, ABS, YS>(npart, apart, fpart, mine + buf * CH, tx,
+                                                    ty, tz, a.yk, T0);
         else
-          near_chunk<KIND, CH, false, FORM, ABS>(npart, apart, fpart, mine + buf * CH, tx, ty,
-                                                 tz, a.yk);
+          near_chunk<KIND, CH, false, FORM, ABS, YS>(npart, apart, fpart, mine + buf * CH, tx,
+                                                     ty, tz, a.yk, T0);
         if ((++nchunk & (kFoldChunks - 1)) == 0 || !more) {   // fold every kFoldChunks chunks
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
@@ -971,10 +1129,10 @@ __device__ __forceinline__ void near_packed_item(const EvalArgs& a, const int4 i
 }
 
 template <int KIND, int CH, int MINB, int FORM, bool PAR = false, bool BULK = false,
-          int ABS = 0>
+          int ABS = 0, bool YS = false>
 __global__ void __launch_bounds__(kWarps * 32, MINB)
 k_near_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int32_t* poff,
-              const uint8_t* dmask, int* counter) {
+              const uint8_t* dmask, const uint8_t* bys, int* counter) {
   extern __shared__ double4 nsmem[];
   __shared__ uint64_t nbar[kWarps][2];   // BULK: one mbarrier per staging buffer
   double4* smem = nsmem;
@@ -984,11 +1142,31 @@ k_near_packed(EvalArgs a, const int4* __restrict__ items, int n_items, const int
     mbar_init(&nbar[warp][0], 1);
     mbar_init(&nbar[warp][1], 1);
   }
+  const double* T0 = nullptr;
+  if constexpr (YS) {   // the shifted-exp table behind the warps' staging buffers
+    double* tab = reinterpret_cast<double*>(smem + kWarps * NearSmem<CH>::kWarp);
+    for (int i = threadIdx.x; i < 2 * kExp2WK + 1; i += blockDim.x) tab[i] = kExp2W[i];
+    __syncthreads();
+    T0 = tab + kExp2WK;
+  }
   __syncwarp();
   unsigned phase = 0;
-  for (int item = next_item(counter); item < n_items; item = next_item(counter))
-    near_packed_item<KIND, CH, FORM, PAR, BULK, ABS>(a, items[item], poff, dmask, wsm, lane,
-                                                nbar[warp], phase);
+  for (int item = next_item(counter); item < n_items; item = next_item(counter)) {
+    const int4 it = items[item];
+    if constexpr (YS) {
+      // the item's batches all within the table's reach: the YS pair loop
+      bool ok = true;
+#pragma unroll
+      for (int k = 0; k < kGMax; ++k) ok &= k >= it.w || bys[it.z + k] != 0;
+      if (ok) {
+        near_packed_item<KIND, CH, FORM, PAR, BULK, ABS, true>(a, it, poff, dmask, wsm, lane,
+                                                             nbar[warp], phase, T0);
+        continue;
+      }
+    }
+    near_packed_item<KIND, CH, FORM, PAR, BULK, ABS>(a, it, poff, dmask, wsm, lane, nbar[warp],
+                                                     phase);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1006,6 +1184,10 @@ int tune_far_dy() {
   const char* e = std::getenv("BLTC_FAR_DY");
   return e ? std::atoi(e) : 1;   // dy^2 per (target, k2) in shared memory: -0.7% far (measured)
 }
+int tune_yshift() {
+  const char* e = std::getenv("BLTC_YSHIFT");
+  return e ? std::atoi(e) : 1;
+}
 int tune_form() {
   const char* e = std::getenv("BLTC_PFORM");
   return e ? std::atoi(e) : 2;   // FORM 2: -0.9% far, -1.5% near at C4 (measured)
@@ -1022,11 +1204,12 @@ int persistent_grid(K kernel, int threads, size_t smem) {
 }
 
 template <int KIND, int M, int KU = 1, int FORM = 0, int MINB = 2, bool PAR = false,
-          bool DY = false>
+          bool DY = false, bool YS = false>
 void far_packed_launch(const EvalArgs& a, const PackedItems& it, int* counter, cudaStream_t st) {
   const size_t smem =
-      sizeof(double) * kWarps * (FarSmem<M>::kWarp + (DY ? FarSmem<M>::kDy : 0));
-  auto kern = k_far_packed<KIND, M, MINB, KU, FORM, PAR, DY>;
+      sizeof(double) * (kWarps * (FarSmem<M>::kWarp + (DY ? FarSmem<M>::kDy : 0)) +
+                        (YS ? 2 * kExp2WK + 1 : 0));
+  auto kern = k_far_packed<KIND, M, MINB, KU, FORM, PAR, DY, YS>;
   BLTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = persistent_grid(kern, kWarps * 32, smem);
   kern<<<grid, kWarps * 32, smem, st>>>(a, it.items_far, it.n_items, it.poff, counter);
@@ -1074,6 +1257,8 @@ bool far_packed_dispatch(const EvalArgs& a, const PackedItems& it, int* counter,
     case 9:
       // tuned for the benchmark degree: k2 unrolled by 3, FORM 2 (measured)
       if (tune_form() != 2) far_packed_launch<KIND, 9, 1, 0>(a, it, counter, st);
+      else if (KIND == 1 && tune_yshift())   // Yukawa, shifted exponential (YS)
+        far_packed_launch<KIND, 9, 3, 2, 1, false, false, true>(a, it, counter, st);
       else if (KIND == 1)   // Yukawa: one CTA per SM, full register file (C3 far -4%; x9 +10%)
         far_packed_launch<KIND, 9, 3, 2, 1>(a, it, counter, st);
       else if (tune_far_dy())   // k2 fully unrolled: C4 far 687 -> 676 ms (x3: 687, x4: 680)
@@ -1085,16 +1270,18 @@ bool far_packed_dispatch(const EvalArgs& a, const PackedItems& it, int* counter,
   }
 }
 
-template <int KIND, int CH = kNearCh, int FORM = 0, bool PAR = false, int ABS = 0>
+template <int KIND, int CH = kNearCh, int FORM = 0, bool PAR = false, int ABS = 0,
+          bool YS = false>
 void near_packed_launch(const EvalArgs& a, const PackedItems& it, int* counter,
                         cudaStream_t st) {
-  const size_t smem = sizeof(double4) * kWarps * NearSmem<CH>::kWarp;
-  auto kern = tune_near_bulk() ? k_near_packed<KIND, CH, 2, FORM, PAR, true, ABS>
-                               : k_near_packed<KIND, CH, 2, FORM, PAR, false, ABS>;
+  const size_t smem = sizeof(double4) * kWarps * NearSmem<CH>::kWarp +
+                      (YS ? sizeof(double) * (2 * kExp2WK + 1) : 0);
+  auto kern = tune_near_bulk() ? k_near_packed<KIND, CH, 2, FORM, PAR, true, ABS, YS>
+                               : k_near_packed<KIND, CH, 2, FORM, PAR, false, ABS, YS>;
   BLTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = persistent_grid(kern, kWarps * 32, smem);
   kern<<<grid, kWarps * 32, smem, st>>>(a, it.items_near, it.n_items, it.poff, it.dmask,
-                                        counter);
+                                        it.bys, counter);
   BLTC_LAUNCH_CHECK();
 }
 }  // namespace
@@ -1190,11 +1377,12 @@ void build_packed_items(const EvalArgs& a, PackedOrder& order, DBuf<int32_t>& pc
     k_window_fill<<<(int)((nw + 255) / 256), 256, 0, st>>>(nb, poff.p, nw, woff.p, items.p);
     BLTC_LAUNCH_CHECK();
   }
-  dmask.resize(n_direct + 1);
+  dmask.resize(n_direct + 1 + nb);   // entry masks, then the per-batch YS flags
+  out->bys = dmask.p + n_direct + 1;
   if (nb > 0) {
     k_direct_mask<<<(int)((nb + 127) / 128), 128, 0, st>>>(nb, a.G, a.d_ptr, a.d_idx,
                                                             a.clusters, a.bcenter, a.bradius,
-                                                            dmask.p);
+                                                            dmask.p, a.yk.c2, dmask.p + n_direct + 1);
     BLTC_LAUNCH_CHECK();
     if (std::getenv("BLTC_TRACE_MASK")) {   // diagnostic: share of masked entries
       std::vector<uint8_t> hm(n_direct);
@@ -1268,7 +1456,8 @@ void launch_eval_packed(const EvalArgs& a, int kind, const PackedItems& it, int*
       else if (v == 2) near_packed_launch<0, kNearCh, 2, false, 2>(a, it, counters + 1, st);
       else near_packed_launch<0, kNearCh, 2, false, 3>(a, it, counters + 1, st);
     } else {
-      if (v == 1) near_packed_launch<1, kNearCh, 2, false, 1>(a, it, counters + 1, st);
+      if (v == 1 && tune_yshift()) near_packed_launch<1, kNearCh, 2, false, 1, true>(a, it, counters + 1, st);
+      else if (v == 1) near_packed_launch<1, kNearCh, 2, false, 1>(a, it, counters + 1, st);
       else if (v == 2) near_packed_launch<1, kNearCh, 2, false, 2>(a, it, counters + 1, st);
       else near_packed_launch<1, kNearCh, 2, false, 3>(a, it, counters + 1, st);
     }
@@ -1277,6 +1466,7 @@ void launch_eval_packed(const EvalArgs& a, int kind, const PackedItems& it, int*
     else near_packed_launch<1>(a, it, counters + 1, st);
   } else {
     if (kind == 0) near_packed_launch<0, kNearCh, 2>(a, it, counters + 1, st);
+    else if (tune_yshift()) near_packed_launch<1, kNearCh, 2, false, 0, true>(a, it, counters + 1, st);
     else near_packed_launch<1, kNearCh, 2>(a, it, counters + 1, st);
   }
   if (timing) {

@@ -126,12 +126,17 @@ class Context:
     """One libbltc context (device buffers + stream) on one CUDA device."""
 
     def __init__(self, device: int = -1, stream: int | None = None):
+        """``stream``: None -- libbltc creates its own (non-blocking) stream;
+        otherwise a CUDA stream handle, e.g. torch.cuda.current_stream().
+        cuda_stream, whose value 0 means the legacy default stream (passed to
+        libbltc as cudaStreamLegacy, so it really runs on that stream)."""
         self._lib = _lib.load()
         h = ctypes.c_void_p()
-        _lib.check(self._lib.bltc_create(int(device), ctypes.c_void_p(stream or 0),
-                                         ctypes.byref(h)))
+        handle = 0 if stream is None else (int(stream) or 1)   # 1 = cudaStreamLegacy
+        _lib.check(self._lib.bltc_create(int(device), ctypes.c_void_p(handle), ctypes.byref(h)))
         self.handle = h
-        self.stream = stream or 0   # the CUDA stream handle libbltc runs on (0: its own)
+        # the torch-visible handle of the stream libbltc runs on (None: its own)
+        self.stream = None if stream is None else int(stream)
 
     def close(self):
         if getattr(self, "handle", None):

@@ -30,6 +30,8 @@ import os
 import sys
 import types
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
@@ -71,8 +73,17 @@ def _make_substitutes():
             raise ref_moments.IneligibleCluster(
                 f"cluster {cluster.index} has a degenerate box extent; "
                 "it is evaluated directly, never approximated")
-        rows = stages.compute_moments(tree, _cfg(int(cluster.grids[0].degree)),
-                                      [cluster.index])
+        # the one cluster as a one-node flat tree: a hand-built cluster over
+        # a SimpleNamespace(points, charges) needs no SourceTree around it
+        f64 = lambda v: np.ascontiguousarray(v, dtype=np.float64)  # noqa: E731
+        i64 = lambda v: np.ascontiguousarray(v, dtype=np.int64)    # noqa: E731
+        one = stages.FlatTree(start=i64([cluster.start]), stop=i64([cluster.stop]),
+                              lo=f64(cluster.box.lo).reshape(1, 3),
+                              hi=f64(cluster.box.hi).reshape(1, 3),
+                              child_start=i64([0]), child_count=i64([0]),
+                              x=f64(tree.points.x), y=f64(tree.points.y), z=f64(tree.points.z),
+                              q=f64(tree.charges))
+        rows = stages.compute_moments(one, _cfg(int(cluster.grids[0].degree)), [0])
         return ref_moments.ClusterMoments(cluster.index, rows[0].copy())
 
     def compute_all_moments(tree):
