@@ -242,24 +242,24 @@ class CpuReference:
                 "est_step_s": est}
 
 
-    def sampled_parity(self, phi_parity, phi_fast) -> dict:
+    def sampled_parity(self, phi_parity, phi_mode) -> dict:
         """Full-size parity on the sampled batches: the CPU restatement's
         potentials of every target in the evaluated sample against the GPU's
-        PARITY (bitwise expected) and FAST results."""
+        PARITY (bitwise expected) and measured-mode (STRICT / FAST) results."""
         b = self.batches
         pos = np.concatenate([np.arange(b.start[i], b.stop[i]) for i in self.sel])
         out, carry = self.last
         ref = (out + carry)[pos]
         orig = b.tree.order[pos]
         dp = np.abs(phi_parity[orig] - ref)
-        df = np.abs(phi_fast[orig] - ref)
+        df = np.abs(phi_mode[orig] - ref)
         nz = ref != 0
         return {"targets": int(pos.shape[0]), "batches": int(len(self.sel)),
                 "parity_bitwise_equal": bool(np.array_equal(phi_parity[orig], ref)),
                 "parity_max_abs_diff": float(dp.max()),
-                "fast_condition_aware": float(df.max() / np.abs(ref).max()),
-                "fast_strict_max_rel": float((df[nz] / np.abs(ref[nz])).max()),
-                "fast_frac_targets_above_1e-10": float((df[nz] / np.abs(ref[nz]) > 1e-10).mean())}
+                "mode_condition_aware": float(df.max() / np.abs(ref).max()),
+                "mode_strict_max_rel": float((df[nz] / np.abs(ref[nz])).max()),
+                "mode_frac_targets_above_1e-10": float((df[nz] / np.abs(ref[nz]) > 1e-10).mean())}
 
 
 def cpu_model() -> str:
@@ -312,7 +312,22 @@ def accuracy_block(ctx, system, econf, mode, phi, args, cpu_ref=None) -> dict:
     sampled = None
     if cpu_ref is not None and getattr(cpu_ref, "last", None) is not None:
         sampled = cpu_ref.sampled_parity(phi_p, phi)
+    # the accuracy cost of the batch size: the same mode at the reference's
+    # default N_L = N_B = 2000 (engine.py:52-53), same verification sample
+    at_default = None
+    if econf.batch_size != 2000 or econf.leaf_size != 2000:
+        from paper_2003_01836_b200 import EvalConfig
+        dconf = EvalConfig(theta=econf.theta, degree=econf.degree, leaf_size=2000,
+                           batch_size=2000, kernel=econf.kernel)
+        t0 = time.perf_counter()
+        phi_d, _ = ctx.treecode(system, dconf, mode=mode)
+        at_default = {"leaf_size": 2000, "batch_size": 2000,
+                      "error": cli.relative_error(ds, phi_d[sample]),
+                      "wall_s_untimed_single_call": time.perf_counter() - t0,
+                      "note": "the timed workload's N_B trades accuracy for speed; "
+                              "profiles/r2_nb_table.jsonl has time and error per N_B"}
     return {"sample": int(sample.shape[0]), "error": err, "error_parity_mode": err_p,
+            "error_at_reference_default_batch": at_default,
             "full_size_parity_vs_cpu_reference": sampled,
             "error_ratio": err / err_p if err_p else None,
             "vs_parity_strict_max_rel": strict,

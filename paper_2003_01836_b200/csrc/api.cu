@@ -488,6 +488,16 @@ void run_moments(bltc_ctx* c, const bltc_params* p, const double* x, const doubl
 // Moments of the flagged clusters of one source tree (moments.py:147-150).
 // all: 0 = clusters on some approximation list, 1 = every eligible cluster,
 // 2 = every cluster the MAC could accept (eligible and (n+1)^3 < N_C).
+// The pad double of each moment row (mstride = (n+1)^3 rounded up to even,
+// for 16-byte copies) is never written by the upward pass; zero it so the
+// evaluation kernels' 16-byte row copies read initialised memory.
+void zero_row_pads(double* rows, int64_t n_rows, int degree, int mstride, cudaStream_t st) {
+  const int64_t m3 = (int64_t)(degree + 1) * (degree + 1) * (degree + 1);
+  if (n_rows <= 0 || mstride == m3) return;
+  BLTC_CUDA(cudaMemset2DAsync(rows + m3, mstride * sizeof(double), 0,
+                              (mstride - m3) * sizeof(double), n_rows, st));
+}
+
 void compute_moments(bltc_ctx* c, const bltc_params* p, const Partition& T, const MacNode* mac,
                      EvalCluster* ecl, int all, DBuf<double>& rows, int64_t cluster_base) {
   cudaStream_t st = c->st;
@@ -518,6 +528,7 @@ void compute_moments(bltc_ctx* c, const bltc_params* p, const Partition& T, cons
   c->mlist.resize(c->n_moments + 1);
   const int mstride = moment_stride(p->degree);
   rows.resize(c->n_moments * mstride + 2);
+  zero_row_pads(rows.p, c->n_moments, p->degree, mstride, st);
   k_compact_moments<<<grid_for(nn, 256), 256, 0, st>>>(nn, c->mflag.p, c->mpos.p, c->mlist.p,
                                                        ecl);
   BLTC_LAUNCH_CHECK();
@@ -1625,6 +1636,7 @@ int bltc_stage_moments(bltc_ctx* c, const bltc_params* p, const double* cheb_s, 
     const int64_t m3 = (int64_t)m * m * m;
     const int mstride = moment_stride(p->degree);
     c->rows.resize(n_list * mstride + 2);
+    zero_row_pads(c->rows.p, n_list, p->degree, mstride, st);
     run_moments(c, p, S.x.p, S.y.p, S.z.p, S.q.p, c->mlist.p, n_list, S.start.p, S.stop.p,
                 S.lo.p, S.hi.p, mstride, c->rows.p);
     BLTC_CUDA(cudaMemcpy2DAsync(rows_out, m3 * sizeof(double), c->rows.p,
