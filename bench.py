@@ -482,9 +482,17 @@ def run_ours(args, cfg):
             ctx.treecode(psys, econf, mode=mode, out=out)
         t1 = time.perf_counter()
         e2e_s = (t1 - t0) / args.steps
+        # the same call with the caller's ordinary (pageable) numpy arrays, as
+        # a reference-side caller passes them (the driver's e2e is pinned)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            bltc.treecode_potentials(system, econf, mode=mode, context=ctx)
+        e2e_pageable_s = (time.perf_counter() - t0) / args.steps
         e2e = {"value": n / e2e_s, "unit": "particles/s", "h2d_bytes_per_step": 4 * 8 * n,
                "d2h_bytes_per_step": 8 * n, "ms_per_step": 1e3 * e2e_s,
-               "api": "paper_2003_01836_b200.treecode_potentials -> bltc_treecode (C ABI)"}
+               "api": "paper_2003_01836_b200.treecode_potentials -> bltc_treecode (C ABI)",
+               "host_buffers": "pinned",
+               "pageable_ms_per_step": 1e3 * e2e_pageable_s}
     else:
         # run_distributed: host arrays in, RCB on the host, H2D of the rank's
         # slice, device pipeline + NCCL forest all-gather, D2H + gather of phi

@@ -1,8 +1,8 @@
 #!/usr/bin/env python
 """Bitwise upward pass (STRICT / PARITY moments) variants on one workload:
-the big-cluster threshold (BLTC_BW_BIG), thread-block clusters sharing
-factor records (BLTC_MOMENTS_CLUSTER), their ring depth (BLTC_BWC_NS) and
-the mbarrier wait's suspend-time hint (BLTC_BW_SUSPEND_NS).
+the big-cluster threshold (BLTC_BW_BIG).  (Earlier sweeps in
+profiles/r2_moments_sweep*.jsonl also covered a thread-block-cluster /
+DSMEM variant, its ring depth and the mbarrier suspend hint.)
 Prints the precompute (moments) phase per variant, STRICT mode.
 
     python tools/moments_sweep.py --config c4
@@ -30,11 +30,9 @@ def main():
     system = bench.make_system(cfg, device=0)
     ctx = bltc.Context(0)
     ref = None
-    variants = [{}, {"BLTC_MOMENTS_CLUSTER": "1"}, {"BLTC_MOMENTS_CLUSTER": "1", "BLTC_BWC_NS": "2"},
-                {"BLTC_BW_SUSPEND_NS": "0"}]
-    for big in ("32768", "65536", "262144"):
+    variants = [{}]
+    for big in ("32768", "65536", "262144", "524288"):
         variants.append({"BLTC_BW_BIG": big})
-        variants.append({"BLTC_BW_BIG": big, "BLTC_MOMENTS_CLUSTER": "1"})
     for v in variants:
         os.environ.update(v)
         ts = []

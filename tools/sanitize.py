@@ -6,7 +6,7 @@
 
 PARITY / FAST / STRICT (forced recompute too), Coulomb / Yukawa, packed and
 per-batch kernels, near-field bulk staging, the bitwise upward pass with its
-big-cluster thread-block-cluster kernel forced on (BLTC_BW_BIG), simulated
+big-cluster split items forced on (BLTC_BW_BIG), simulated
 ranks (multi-group forest), the direct-sum oracle and the C host ABI paths."""
 import os
 import sys
@@ -53,10 +53,6 @@ ctx.direct_sum(s, bltc.coulomb(), np.arange(0, 6000, 37), mode="fast")
 cfg = bltc.EvalConfig(theta=0.8, degree=3, leaf_size=200, batch_size=200,
                       kernel=bltc.test_constant())
 ctx.treecode(u, cfg, mode="strict")
-os.environ["BLTC_MOMENTS_CLUSTER"] = "1"   # the DSMEM thread-block-cluster upward pass
-for mode in ("parity", "strict"):
-    ctx.treecode(s, bltc.EvalConfig(theta=0.8, degree=8, leaf_size=400, batch_size=160), mode=mode)
-del os.environ["BLTC_MOMENTS_CLUSTER"]
 # Yukawa: shifted-exponential (YS) far / near kernels and their fallbacks
 for kappa in (0.5, 40.0):
     ycfg = bltc.EvalConfig(theta=0.7, degree=8, leaf_size=500, batch_size=160,
