@@ -141,15 +141,18 @@ def rcb_partition(points: Points, ranks: int) -> RcbPartition:
 class DeviceRcb:
     """RCB on the device (FAST runs): the same cuts, axes and per-rank counts
     as rcb_partition (decomp.py:76-130) -- exact order statistics, floor/ceil
-    shares, the longest slab extent, ties to the lowest axis -- but each cut
-    is a stable device sort instead of numpy's argpartition, so the order of
-    particles WITHIN a rank differs from the reference's (tree shapes and
-    cluster memberships do not; only summation order in FAST sums does).
-    ``order`` stays on the device.  When particles share the coordinate at a
-    cut's order statistic, the stable sort and numpy's introselect may put
-    different tied particles on the left: ``tied`` is then True and callers
-    fall back to the host rcb_partition (so each rank still gets exactly the
-    reference's particle set)."""
+    shares, the longest slab extent, ties to the lowest axis.  Each cut is a
+    selection, not a sort: ``torch.kthvalue`` finds the n_left-th and
+    (n_left+1)-th smallest coordinates (left_max, right_min), and an
+    order-preserving compaction splits the slab at them -- O(n) per cut and
+    one small host read (the two order statistics, which also give the cut
+    plane).  Each rank gets exactly the reference's particle SET; the order
+    within a rank is the input order (the reference's argpartition order
+    differs), which only changes FAST summation order.  ``order`` stays on
+    the device.  When particles share the coordinate at a cut's order
+    statistic the reference's introselect decides which tied particles go
+    left: ``tied`` is then True and callers fall back to the host
+    rcb_partition."""
 
     def __init__(self, x, y, z, ranks: int):
         import torch
@@ -159,8 +162,8 @@ class DeviceRcb:
         if n < ranks:
             raise ValueError(f"need at least one particle per rank ({n} < {ranks})")
         coords = (x, y, z)
-        lo = np.array([float(c.min().item()) for c in coords])
-        hi = np.array([float(c.max().item()) for c in coords])
+        ext = torch.stack([torch.stack([c.min(), c.max()]) for c in coords]).cpu().numpy()
+        lo, hi = ext[:, 0].copy(), ext[:, 1].copy()
         self.order = torch.arange(n, device=x.device)
         self.tied = False
         shares = np.array([(n * (r + 1)) // ranks - (n * r) // ranks for r in range(ranks)],
@@ -168,19 +171,21 @@ class DeviceRcb:
         self.rank_start = np.concatenate(([0], np.cumsum(shares)))
 
         def recurse(start, stop, r0, r1, lo, hi):
-            if r1 - r0 == 1:
+            if r1 - r0 == 1 or self.tied:
                 return
             rm = r0 + (r1 - r0) // 2
             n_left = int(shares[r0:rm].sum())
             axis = _cut_axis(lo, hi)
             idx = self.order[start:stop]
             vals = coords[axis][idx]
-            perm = torch.argsort(vals, stable=True)
-            self.order[start:stop] = idx[perm]
-            sv = vals[perm]
-            left_max, right_min = (float(v) for v in sv[[n_left - 1, n_left]].tolist())
+            stats = torch.stack([torch.kthvalue(vals, n_left).values,
+                                 torch.kthvalue(vals, n_left + 1).values])
+            left_max, right_min = (float(v) for v in stats.cpu().tolist())
             if left_max == right_min:
                 self.tied = True
+                return
+            go_left = vals <= left_max   # exactly n_left: no value sits in between
+            self.order[start:stop] = torch.cat([idx[go_left], idx[~go_left]])
             cut = 0.5 * (left_max + right_min)
             lo_hi = hi.copy()
             lo_hi[axis] = cut

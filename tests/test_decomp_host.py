@@ -201,7 +201,7 @@ def test_single_process_let_matches_reference_fetch():
 
 def test_device_rcb_flags_ties_at_a_cut():
     """DeviceRcb (torch, here on CPU tensors) takes the reference's cuts with
-    stable sorts; when particles share the coordinate at a cut's order
+    order-statistic selection; when particles share the coordinate at a cut's order
     statistic it flags ``tied`` (run_distributed then uses the reference's
     own rcb_partition), and on continuous data it reproduces the reference's
     rank SETS exactly."""

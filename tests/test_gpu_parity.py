@@ -43,14 +43,12 @@ def _phi_check(phi, ref, kind, exact):
     if exact:
         np.testing.assert_array_equal(phi, ref)
     else:
-        # FAST (uncertified): condition-aware bar, and the per-target bar away
-        # from near-cancelling targets; STRICT mode meets the per-target bar
-        # on every target (tests/test_gpu_strict.py)
+        # FAST is the uncertified mode: its contract is the condition-aware
+        # bar (|d_i| <= 1e-13 max |phi|), NOT the per-target one -- a near-
+        # cancelling target can exceed 1e-10 relative.  The per-target bar on
+        # EVERY target (no masking) is STRICT's: tests/test_gpu_strict.py.
         scale = np.abs(ref).max()
         assert np.abs(phi - ref).max() <= 1e-13 * scale
-        rel = np.abs(phi - ref) / np.abs(ref)
-        ok = np.abs(ref) > 1e-3 * np.sqrt(np.mean(ref ** 2))
-        assert rel[ok].max() <= 1e-10
 
 
 @pytest.mark.parametrize("case", CASES)

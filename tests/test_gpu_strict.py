@@ -82,18 +82,21 @@ def test_strict_kc_zero_recomputes_nothing(bltc, monkeypatch):
     assert np.abs(phi - ref).max() <= 1e-13 * np.abs(ref).max()
 
 
-@pytest.mark.parametrize("gen,n,leaf,batch,deg,theta,kind", [
-    ("uniform", 200_000, 2000, 160, 8, 0.8, 0),
-    ("plummer", 200_000, 2000, 160, 8, 0.8, 0),
-    ("uniform", 150_000, 2000, 160, 10, 0.7, 0),
-    ("uniform", 150_000, 2000, 160, 8, 0.8, 1),
+@pytest.mark.parametrize("gen,n,leaf,batch,deg,theta,kind,kappa", [
+    ("uniform", 200_000, 2000, 160, 8, 0.8, 0, 0.0),
+    ("plummer", 200_000, 2000, 160, 8, 0.8, 0, 0.0),
+    ("uniform", 150_000, 2000, 160, 10, 0.7, 0, 0.0),
+    ("uniform", 150_000, 2000, 160, 8, 0.8, 1, 0.5),
+    # Yukawa far / near beyond the shifted-exp table's reach: the generic
+    # exponential fallbacks (eval_packed.cu far_cluster_generic, bys flags)
+    ("uniform", 60_000, 1000, 160, 8, 0.8, 1, 6.0),
+    ("plummer", 60_000, 1000, 160, 8, 0.8, 1, 40.0),
 ])
-def test_strict_mid_size_vs_oracle(bltc, oracle, gen, n, leaf, batch, deg, theta, kind):
+def test_strict_mid_size_vs_oracle(bltc, oracle, gen, n, leaf, batch, deg, theta, kind, kappa):
     import os
     from paper_2003_01836_b200 import cli
     s = (cli.generate_particles if gen == "uniform" else cli.generate_plummer)(n, 4)
     src = s.sources
-    kappa = 0.5 if kind == 1 else 0.0
     ref, _ = oracle.treecode_potentials(src.x, src.y, src.z, src.x, src.y, src.z, s.charges,
                                         True, theta, deg, leaf, batch, kind, kappa,
                                         threads=os.cpu_count() or 1)
