@@ -62,6 +62,11 @@ def main():
                                 else ours.coulomb())
         phi_p, _ = ours.treecode_potentials(mine, oconf, mode="parity")
         out["gpu_parity_bitwise_equal"] = bool(np.array_equal(phi_p, phi))
+        phi_s, _ = ours.treecode_potentials(mine, oconf, mode="strict")
+        d = np.abs(phi_s - phi)
+        nz = phi != 0
+        out["gpu_strict_max_rel"] = float((d[nz] / np.abs(phi[nz])).max())
+        out["gpu_strict_targets_above_1e-10"] = int((d[nz] > 1e-10 * np.abs(phi[nz])).sum())
     except Exception as exc:   # reported, not required
         out["gpu_parity_bitwise_equal"] = repr(exc)
     print(json.dumps(out), flush=True)
