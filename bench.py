@@ -339,9 +339,10 @@ def accuracy_block(ctx, system, econf, mode, phi, args, cpu_ref=None) -> dict:
 
 
 def run_reference(args, cfg):
-    """--impl reference: the reference's CPU algorithm (oracle port; the
-    Python/numba reference itself is not installable on the box) on this
-    host's cores, each step a bounded sample of the same workload."""
+    """--impl reference: the reference's CPU algorithm (oracle/'s C port: the
+    reference is Python/numba, not a compiled library -- its own timing on
+    the same host is anchored separately, tools/reference_numba_step.py) on
+    this host's cores, each step a bounded sample of the same workload."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -370,7 +371,10 @@ def run_reference(args, cfg):
                          "cpu_model": res["cpu_model"],
                          "sampled_pair_fraction": res["sampled_pair_fraction"],
                          "anchor": "profiles/r2_cpu_full_step_*.json: unsampled full steps of "
-                                   "the same C port, checking the extrapolation"},
+                                   "the same C port, checking the extrapolation; "
+                                   "profiles/r2_reference_numba_*.json: the unmodified numba "
+                                   "reference on the same host (C4: 410.4 s per step on 16 "
+                                   "threads, 1.5x slower than this port)"},
         "e2e": {"value": value, "unit": "particles/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
