@@ -25,4 +25,5 @@ def test_c_host_program(tmp_path):
     assert r.returncode == 0, r.stdout + r.stderr
     out = json.loads(r.stdout.strip().splitlines()[-1])
     assert out["rel_l2_error"] < 1e-4 and out["fast_vs_parity"] < 1e-13
+    assert out["strict_max_rel"] <= 1e-10
     assert out["ranks2_rel_l2_error"] < 1e-4

@@ -40,9 +40,12 @@ BLTC_BENCH_SHARE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
   --clock-control none --csv --log-file gpurun_out/launches_c4_strict.csv \
   python tools/one_step.py --config c4 --steps 2 --mode strict > gpurun_out/launches_c4.log 2>&1
+# (reports summarised on the box and deleted: gpurun returns <= 64 MiB)
 for k in k_far_packed k_near_packed k_moments_bw k_strict_recompute; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -c 1 \
-    -o gpurun_out/ncu_$k python tools/one_step.py --config c4 --steps 1 --mode strict > gpurun_out/ncu_$k.log 2>&1
+    -o /tmp/ncu_$k python tools/one_step.py --config c4 --steps 1 --mode strict > gpurun_out/ncu_$k.log 2>&1
+  python tools/ncu_summary.py /tmp/ncu_$k.ncu-rep gpurun_out/ncu_${k}_c4.txt > /dev/null 2>&1
 done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_far_packed -c 1 \
-  -o gpurun_out/ncu_far_yukawa_c3 python tools/one_step.py --config c3 --steps 1 --mode strict > gpurun_out/ncu_far_c3.log 2>&1
+  -o /tmp/ncu_far_c3 python tools/one_step.py --config c3 --steps 1 --mode strict > gpurun_out/ncu_far_c3.log 2>&1
+python tools/ncu_summary.py /tmp/ncu_far_c3.ncu-rep gpurun_out/ncu_far_yukawa_c3.txt > /dev/null 2>&1
