@@ -3,12 +3,15 @@
 Runs the distributed pipeline of decomp.run_distributed rank by rank on one
 device (one libbltc context per rank), timing each rank's phases with CUDA
 events: build (tree, batches, moments), publish, LET step one (needs),
-serve + assemble of the fetched rows / slices, evaluate.  The projected
-R-GPU step is the max over ranks of the rank's device time plus the
-exchange volume over NVLink at an assumed 400 GB/s per GPU with 4
-collectives of 30 us latency.  This is a projection, not a measurement.
+serve + assemble of the fetched rows / slices, evaluate.  With
+``--exchange replicate`` (bench.py's N > 1 default: one packed all-gather of
+every rank's forest) the LET steps are skipped and every rank evaluates
+against the whole forest.  The projected R-GPU step is the max over ranks
+of the rank's device time plus the exchange volume over NVLink at an
+assumed 400 GB/s per GPU with 4 (LET) / 2 (replicate) collectives of 30 us
+latency.  This is a projection, not a measurement.
 
-    python tools/sim_ranks.py --config c4 --ranks 2,4,8
+    python tools/sim_ranks.py --config c4 --ranks 2,4,8 [--mode strict] [--exchange replicate]
 """
 import argparse
 import json
@@ -29,6 +32,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c4")
 ap.add_argument("--ranks", default="2,4,8")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--mode", default="strict", choices=["strict", "fast", "parity"])
+ap.add_argument("--exchange", default="replicate", choices=["let", "replicate"])
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
 system = bench.make_system(cfg)
@@ -51,7 +56,7 @@ def timed(fn):
 for R in map(int, args.ranks.split(",")):
     part = rcb_partition(src, R)
     ctxs = [engine.Context(0) for _ in range(R)]
-    engs = [DeviceRankEngine(econf, "fast", context=ctxs[r]) for r in range(R)]
+    engs = [DeviceRankEngine(econf, args.mode, context=ctxs[r]) for r in range(R)]
     inputs = []
     for r in range(R):
         idx = part.rank_indices(r)
@@ -69,7 +74,14 @@ for R in map(int, args.ranks.split(",")):
         ncols = int(pubs[0].moments.shape[1])
         fetched_bytes = {r: 0 for r in range(R)}
         forests = {}
-        for r in range(R):
+        if args.exchange == "replicate":
+            block = {o: sum(int(t.numel()) * 8 for t in (pubs[o].records, pubs[o].particles,
+                                                        pubs[o].moments)) for o in range(R)}
+            for r in range(R):
+                ph[r]["needs_ms"] = ph[r]["let_host_ms"] = 0.0
+                forests[r] = [pubs[o] for o in range(R)]
+                fetched_bytes[r] = sum(block[o] for o in range(R) if o != r)
+        for r in range(R) if args.exchange == "let" else ():
             flags, ph[r]["needs_ms"], _ = timed(lambda: engs[r].needs(R, r, recs))
             t0 = time.perf_counter()
             forest = []
@@ -101,7 +113,10 @@ for R in map(int, args.ranks.split(",")):
         dev = {r: sum(ph[r][k] for k in ("build_ms", "publish_ms", "needs_ms", "let_host_ms",
                                            "evaluate_ms")) for r in range(R)}
         rec_bytes = sum(int(x.numel()) * 8 for x in recs)
-        xfer_ms = max((fetched_bytes[r] + rec_bytes) / 400e9 * 1e3 for r in range(R)) + 4 * 0.03
+        if args.exchange == "replicate":
+            xfer_ms = max(fetched_bytes[r] / 400e9 * 1e3 for r in range(R)) + 2 * 0.03
+        else:
+            xfer_ms = max((fetched_bytes[r] + rec_bytes) / 400e9 * 1e3 for r in range(R)) + 4 * 0.03
         proj = max(dev.values()) + xfer_ms
         if best is None or proj < best["projected_step_ms"]:
             best = {"ranks": R, "projected_step_ms": proj, "max_rank_device_ms": max(dev.values()),
@@ -110,6 +125,7 @@ for R in map(int, args.ranks.split(",")):
                     "fetched_MB_max": max(fetched_bytes.values()) / 1e6,
                     "records_MB": rec_bytes / 1e6, "per_rank": ph}
     print(json.dumps({"config": args.config, "n": cfg["n"], "batch_size": econf.batch_size,
+                      "mode": args.mode, "exchange": args.exchange,
                       **best}), flush=True)
     for c in ctxs:
         c.close()
