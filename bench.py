@@ -530,7 +530,7 @@ def run_ours(args, cfg):
 
     traffic = None
     tp = os.path.join(ROOT, "profiles", "far_traffic.json")
-    if os.path.exists(tp):
+    if world == 1 and os.path.exists(tp):   # a single-device capture
         try:
             with open(tp) as f:
                 tj = json.load(f)
