@@ -384,19 +384,22 @@ __device__ __forceinline__ void far_stage_slab(double* wsm, const FarHdr* H, int
 // no clamp in the pair loop (16 FP64 slots per pair instead of 17, and ~5
 // fewer integer instructions); the 2^(-s/2048) factor is applied once per
 // (target, cluster).  Clusters with c hd + 2 > 2048, or targets with
-// c r_ref >= 2^49, take the generic exp_neg_kr path for that step.
+// c r_ref >= 2^30, take the generic exp_neg_kr path for that step.
 struct YsState {
   double S;    // magic + s
   double E;    // 2^(-s/2048)
+  int si;      // s (< 2^30)
 };
 
-__device__ __forceinline__ double ys_pair_factor(double d2, double c, double S,
+// S - z = s - k is formed in the integer pipe and converted (I2F), not by a
+// DADD on the FP64 pipe: one FP64 slot less per pair.
+__device__ __forceinline__ double ys_pair_factor(double d2, double c, double S, int si,
                                                  const double* __restrict__ T0) {
   const double y = rsqrt_fast(d2);
   const double r = __dmul_rn(d2, y);
   const double z = fma(r, -c, S);
   const int k = __double2loint(z);
-  const double f = fma(r, -c, __dsub_rn(S, z));
+  const double f = fma(r, -c, (double)(si - k));
   constexpr double a1 = 0x1.62e42fefa39efp-12;   // ln2 / 2048
   constexpr double a2 = a1 * a1 / 2.0;
   constexpr double a3 = a1 * a1 * a1 / 6.0;
@@ -415,8 +418,9 @@ __device__ __forceinline__ double ys_pair_factor_near(double d2, double c,
   const double y = rsqrt_fast(d2);
   const double r = __dmul_rn(d2, y);
   const double z = fma(r, -c, kMagic);
-  const int k = -(int)umin((unsigned)(-__double2loint(z)), (unsigned)kExp2WK);   // [-2048, 0]
-  const double f = fma(r, -c, __dsub_rn(kMagic, z));
+  const int kr = __double2loint(z);
+  const int k = -(int)umin((unsigned)(-kr), (unsigned)kExp2WK);   // [-2048, 0]
+  const double f = fma(r, -c, (double)(-kr));   // magic - z = -k, via I2F (see ys_pair_factor)
   constexpr double a1 = 0x1.62e42fefa39efp-12;   // ln2 / 2048
   constexpr double a2 = a1 * a1 / 2.0;
   constexpr double a3 = a1 * a1 * a1 / 6.0;
@@ -432,10 +436,11 @@ __device__ __forceinline__ YsState ys_state(double tx, double ty, double tz, dou
   const double kMagic = 6755399441055744.0;   // 1.5 * 2^52
   const double dx = tx - cx, dy = ty - cy, dz = tz - cz;
   const double u = c * sqrt(fma(dx, dx, fma(dy, dy, dz * dz)));
-  ok = u < 0x1p49;
+  ok = u < 0x1p30;
   const double sd = ok ? rint(u) : 0.0;
   YsState st;
   st.S = kMagic + sd;
+  st.si = (int)sd;
   // 2^(-s/2048) = 2^(-m) T[-j], s = 2048 m + j, 0 <= j < 2048
   const long long si = (long long)sd;
   const int j = (int)(si & 2047);
@@ -623,7 +628,7 @@ __device__ __forceinline__ void far_packed_item(const EvalArgs& a, const int4 it
             } else if (PAR) {
               part[t] = __dadd_rn(part[t], parity_term<KIND>(qv, d2, a.kappa));
             } else if (YS) {
-              part[t] = fma(qv, ys_pair_factor(d2, a.yk.c2, ys[t].S, T0), part[t]);
+              part[t] = fma(qv, ys_pair_factor(d2, a.yk.c2, ys[t].S, ys[t].si, T0), part[t]);
             } else {
               part[t] = pair_acc<KIND, FORM>(part[t], qv, d2, a.yk);
             }
