@@ -61,6 +61,14 @@ CONFIGS = {
                batch=160),
     "c4u": dict(workload="N=8M uniform cube, Coulomb, n=8, theta=0.8", gen="uniform",
                 n=8_000_000, kind=0, kappa=0.0, degree=8, theta=0.8, leaf=2000, batch=2000),
+    # accuracy context for the north star's "~1e-7 relative error" at 8M: the
+    # same cube / Plummer sphere at C5's n = 10, theta = 0.7
+    "c4u_n10": dict(workload="N=8M uniform cube, Coulomb, n=10, theta=0.7", gen="uniform",
+                    n=8_000_000, kind=0, kappa=0.0, degree=10, theta=0.7, leaf=2000,
+                    batch=160),
+    "c4_n10": dict(workload="N=8M Plummer (a=1, r<=10a), Coulomb, n=10, theta=0.7",
+                   gen="plummer", n=8_000_000, kind=0, kappa=0.0, degree=10, theta=0.7,
+                   leaf=2000, batch=160),
     # C5: N_B=160 (level-7 batches): 10.1 s vs 11.2 s at 250 and 11.7 s at 1000
     "c5": dict(workload="C5: N=64M uniform cube, Coulomb, n=10, theta=0.7", gen="uniform",
                n=64_000_000, kind=0, kappa=0.0, degree=10, theta=0.7, leaf=2000, batch=160),
