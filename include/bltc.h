@@ -247,6 +247,11 @@ typedef struct {
 BLTC_API int bltc_rank_build(bltc_ctx* ctx, const bltc_params* p, const double* cheb_s, int64_t n,
                     const double* x, const double* y, const double* z, const double* q,
                     int32_t device_ptrs);
+/* Optional, before bltc_rank_build: the bounding box of ALL ranks' targets
+ * (lo[3], hi[3]).  The rank then computes and publishes moment rows only for
+ * clusters some batch inside that box could accept (r_C / theta reachable,
+ * engine.py:65-85); NULL restores "every cluster that passes the size test". */
+BLTC_API int bltc_rank_set_domain(bltc_ctx* ctx, const double* lo, const double* hi);
 BLTC_API int bltc_rank_publish_sizes(bltc_ctx* ctx, bltc_publish_sizes* out);
 /* records: [n_clusters][record_doubles]; particles: [4][n_particles] (x,y,z,q);
  * moments: [n_moment_rows][(n+1)^3 rounded up to even].  All device pointers. */

@@ -85,6 +85,8 @@ SIGNATURES = {
     "bltc_export_moments": (ctypes.c_int, [_vp, _i64p, _f64p]),
     "bltc_rank_build": (ctypes.c_int, [_vp, ctypes.POINTER(Params), _f64p, ctypes.c_int64, _vp,
                                        _vp, _vp, _vp, ctypes.c_int32]),
+    "bltc_rank_set_domain": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_double),
+                                            ctypes.POINTER(ctypes.c_double)]),
     "bltc_rank_publish_sizes": (ctypes.c_int, [_vp, ctypes.POINTER(PublishSizes)]),
     "bltc_rank_publish": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "bltc_rank_evaluate": (ctypes.c_int, [_vp, ctypes.POINTER(Params), ctypes.c_int32,

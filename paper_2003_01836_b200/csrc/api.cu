@@ -115,14 +115,36 @@ __global__ void k_batches(int64_t nb, const int32_t* leaves, const double* lo, c
   bstop[b] = stop[i];
 }
 
+// all == 2 (a rank's publishable rows): every eligible cluster that passes
+// the size test and that some batch of the global domain [dlo, dhi] could
+// accept geometrically -- a batch ball centred in the domain accepts cluster
+// c only if r_B + r_C <= theta |B - C| (engine.py:65-85), so |B - C| >=
+// r_C / theta must be reachable inside the domain (dom = nullptr: no filter).
 __global__ void k_flag_moments(int64_t nn, const MacNode* nodes, int64_t per_node, int all,
-                               const int32_t* used, int32_t* flag) {
+                               const int32_t* used, int32_t* flag, const double* dom,
+                               double theta) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nn) return;
   int f;
-  if (all == 1) f = nodes[i].eligible;                                  // compute_all_moments
-  else if (all == 2) f = nodes[i].eligible && per_node < nodes[i].count;  // any possible approx
-  else f = used[i];
+  if (all == 1) {
+    f = nodes[i].eligible;                                  // compute_all_moments
+  } else if (all == 2) {
+    const MacNode& m = nodes[i];
+    f = m.eligible && per_node < m.count;                   // any possible approx
+    if (f && dom) {
+      const double c[3] = {m.cx, m.cy, m.cz};
+      double far2 = 0.0;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double e = fmax(fabs(dom[d] - c[d]), fabs(dom[3 + d] - c[d]));
+        far2 += e * e;
+      }
+      // generous margins: a cluster on the edge of reach keeps its row
+      f = sqrt(far2) * (1.0 + 1e-9) * theta >= m.radius * (1.0 - 1e-9);
+    }
+  } else {
+    f = used[i];
+  }
   flag[i] = f;
 }
 
@@ -231,6 +253,11 @@ struct bltc_ctx {
   int device = 0;
   cudaStream_t st = nullptr;
   bool own_stream = false;
+  // bltc_rank_set_domain: the global domain, to skip moment rows no batch
+  // anywhere could read
+  bool has_domain = false;
+  double domain[6] = {0, 0, 0, 0, 0, 0};
+  DBuf<double> domain_dev;
   bool timing = true;
   HostScratch hs;
   BuildScratch bs;
@@ -517,7 +544,15 @@ void compute_moments(bltc_ctx* c, const bltc_params* p, const Partition& T, cons
     }
   }
   (void)cluster_base;
-  k_flag_moments<<<grid_for(nn, 256), 256, 0, st>>>(nn, mac, m3, all, c->used.p, c->mflag.p);
+  const double* dom = nullptr;
+  if (all == 2 && c->has_domain) {
+    c->domain_dev.resize(6);
+    BLTC_CUDA(cudaMemcpyAsync(c->domain_dev.p, c->domain, 6 * sizeof(double),
+                              cudaMemcpyHostToDevice, st));
+    dom = c->domain_dev.p;
+  }
+  k_flag_moments<<<grid_for(nn, 256), 256, 0, st>>>(nn, mac, m3, all, c->used.p, c->mflag.p, dom,
+                                                    p->theta);
   BLTC_LAUNCH_CHECK();
   BLTC_CUDA(cudaMemsetAsync(c->mflag.p + nn, 0, sizeof(int32_t), st));
   exclusive_scan_i32(c->mflag.p, c->mpos.p, nn + 1, c->bs.scan_tmp, st);
@@ -984,6 +1019,7 @@ int bltc_destroy(bltc_ctx* c) {
     c->f_y.release(); c->f_z.release(); c->f_q.release(); c->f_rows.release();
     c->f_src4.release();
     c->hs.release();
+    c->domain_dev.release();
     if (c->own_stream) cudaStreamDestroy(c->st);
     delete c;
   });
@@ -1317,6 +1353,25 @@ int bltc_rank_build(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int
     BLTC_CUDA(cudaStreamSynchronize(st));
     c->rank_n = n;
     c->rank_built = true;
+  });
+}
+
+int bltc_rank_set_domain(bltc_ctx* c, const double* lo, const double* hi) {
+  return guarded([&] {
+    if (!c) throw UserError{BLTC_ERR_VALUE};
+    if (!lo || !hi) {
+      c->has_domain = false;
+      return;
+    }
+    for (int d = 0; d < 3; ++d) {
+      if (!std::isfinite(lo[d]) || !std::isfinite(hi[d]) || lo[d] > hi[d]) {
+        set_error("domain bounds must be finite with lo <= hi");
+        throw UserError{BLTC_ERR_VALUE};
+      }
+      c->domain[d] = lo[d];
+      c->domain[3 + d] = hi[d];
+    }
+    c->has_domain = true;
   });
 }
 

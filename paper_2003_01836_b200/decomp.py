@@ -634,9 +634,16 @@ class DeviceRankEngine:
         self.n = 0
         self.stats = None
 
+    def set_domain(self, lo, hi) -> None:
+        """The bounding box of ALL ranks' targets: moment rows no batch in it
+        could read are not computed or published (bltc_rank_set_domain)."""
+        self.domain = (np.asarray(lo, dtype=np.float64), np.asarray(hi, dtype=np.float64))
+
     def build(self, x, y, z, q) -> None:
         torch = self.torch
         dev = torch.device("cuda", self.device)
+        dom = getattr(self, "domain", None)
+        self.ctx.rank_set_domain(*(dom if dom is not None else (None, None)))
         self._inputs = [torch.as_tensor(np.ascontiguousarray(v, dtype=np.float64)
                                         if not isinstance(v, torch.Tensor) else v,
                                         device=dev).contiguous() for v in (x, y, z, q)]
@@ -818,6 +825,12 @@ def run_distributed(system, config, ranks: int, threads: int = 1, mode: str | No
     src = system.sources
     x, y, z = np.asarray(src.x), np.asarray(src.y), np.asarray(src.z)
     q = np.asarray(system.charges)
+    if len(x):
+        lo = np.array([x.min(), y.min(), z.min()])
+        hi = np.array([x.max(), y.max(), z.max()])
+        for e in engines.values():
+            if hasattr(e, "set_domain"):
+                e.set_domain(lo, hi)
     if on_device:
         dev = torch.device("cuda", torch.cuda.current_device())
         x, y, z, q = (torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(dev)
@@ -925,6 +938,8 @@ class DeviceRankRunner:
         self.inputs = [torch.from_numpy(np.ascontiguousarray(np.asarray(a)[idx])).to(dev)
                        for a in (src.x, src.y, src.z, system.charges)]
         self.engine = DeviceRankEngine(config, mode, context=ctx)
+        sx, sy, sz = (np.asarray(a) for a in (src.x, src.y, src.z))
+        self.engine.set_domain([sx.min(), sy.min(), sz.min()], [sx.max(), sy.max(), sz.max()])
         self.n_local = int(idx.shape[0])
         self.exchange = exchange
         self.phi = None

@@ -242,6 +242,15 @@ class Context:
                                              _lib.f64p(nodes), int(n), *args,
                                              1 if device_ptrs else 0))
 
+    def rank_set_domain(self, lo, hi) -> None:
+        """The global target domain for the next rank_build (None: unset)."""
+        if lo is None:
+            _lib.check(self._lib.bltc_rank_set_domain(self.handle, None, None))
+            return
+        lo = np.ascontiguousarray(lo, dtype=np.float64)
+        hi = np.ascontiguousarray(hi, dtype=np.float64)
+        _lib.check(self._lib.bltc_rank_set_domain(self.handle, _lib.f64p(lo), _lib.f64p(hi)))
+
     def rank_publish_sizes(self) -> dict:
         ps = _lib.PublishSizes()
         _lib.check(self._lib.bltc_rank_publish_sizes(self.handle, ctypes.byref(ps)))

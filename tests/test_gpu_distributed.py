@@ -171,3 +171,33 @@ def test_c_run_distributed_rejects_bad_partition(bltc):
         2, dev.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), 1, ctypes.byref(p),
         dp(cheb_nodes(2)), 100, dp(x), dp(x), dp(x), dp(x), ip(order), ip(start), dp(phi), None)
     assert rc == -1
+
+
+def test_rank_domain_filter_keeps_results(bltc):
+    """bltc_rank_set_domain: a rank publishes only the moment rows some batch
+    of the global domain could accept -- fewer rows (at R = 1 the root and
+    the other clusters no batch can reach drop out), bitwise the same PARITY
+    potentials as publishing every size-eligible row."""
+    import torch
+
+    from paper_2003_01836_b200 import cli
+    from paper_2003_01836_b200.decomp import DeviceRankEngine
+    s = cli.generate_plummer(60_000, 8)
+    src = s.sources
+    cfg = bltc.EvalConfig(theta=0.8, degree=6, leaf_size=500, batch_size=160)
+    lo = [float(np.min(a)) for a in (src.x, src.y, src.z)]
+    hi = [float(np.max(a)) for a in (src.x, src.y, src.z)]
+    out, rows = {}, {}
+    for filt in (False, True):
+        eng = DeviceRankEngine(cfg, "parity")
+        if filt:
+            eng.set_domain(lo, hi)
+        eng.build(*(np.asarray(a) for a in (src.x, src.y, src.z, s.charges)))
+        pub = eng.publish()
+        rows[filt] = pub.sizes[2]
+        out[filt] = eng.evaluate(1, 0, [pub]).cpu().numpy()
+        eng.ctx.close()
+    assert rows[True] < rows[False]
+    np.testing.assert_array_equal(out[True], out[False])
+    ref, _ = bltc.treecode_potentials(s, cfg, mode="parity")
+    np.testing.assert_array_equal(out[True], ref)

@@ -57,6 +57,10 @@ for R in map(int, args.ranks.split(",")):
     part = rcb_partition(src, R)
     ctxs = [engine.Context(0) for _ in range(R)]
     engs = [DeviceRankEngine(econf, args.mode, context=ctxs[r]) for r in range(R)]
+    dom_lo = [float(np.min(a)) for a in (src.x, src.y, src.z)]
+    dom_hi = [float(np.max(a)) for a in (src.x, src.y, src.z)]
+    for e in engs:
+        e.set_domain(dom_lo, dom_hi)
     inputs = []
     for r in range(R):
         idx = part.rank_indices(r)
