@@ -252,6 +252,16 @@ BLTC_API int bltc_rank_build(bltc_ctx* ctx, const bltc_params* p, const double* 
  * clusters some batch inside that box could accept (r_C / theta reachable,
  * engine.py:65-85); NULL restores "every cluster that passes the size test". */
 BLTC_API int bltc_rank_set_domain(bltc_ctx* ctx, const double* lo, const double* hi);
+/* The same with the domain as a union of n_boxes boxes, boxes[6k..6k+5] =
+ * (lo xyz, hi xyz), every batch centre inside one of them (n_boxes = 0:
+ * unset).  Host pointer; copied. */
+BLTC_API int bltc_rank_set_domain_boxes(bltc_ctx* ctx, int64_t n_boxes, const double* boxes);
+/* Host helper: the minimal bounding boxes of the occupied cells of a grid^3
+ * grid over the points' bounding box (grid <= 64), in cell order; boxes
+ * needs room for 6 grid^3 doubles.  The domain bltc_run_distributed passes
+ * to its ranks (grid 16). */
+BLTC_API int bltc_domain_cells(int64_t n, const double* x, const double* y, const double* z,
+                               int32_t grid, double* boxes, int64_t* n_boxes);
 BLTC_API int bltc_rank_publish_sizes(bltc_ctx* ctx, bltc_publish_sizes* out);
 /* records: [n_clusters][record_doubles]; particles: [4][n_particles] (x,y,z,q);
  * moments: [n_moment_rows][(n+1)^3 rounded up to even].  All device pointers. */

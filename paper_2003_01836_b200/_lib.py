@@ -87,6 +87,12 @@ SIGNATURES = {
                                        _vp, _vp, _vp, ctypes.c_int32]),
     "bltc_rank_set_domain": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_double),
                                             ctypes.POINTER(ctypes.c_double)]),
+    "bltc_rank_set_domain_boxes": (ctypes.c_int, [_vp, ctypes.c_int64,
+                                                  ctypes.POINTER(ctypes.c_double)]),
+    "bltc_domain_cells": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(ctypes.c_double),
+                                         ctypes.POINTER(ctypes.c_double),
+                                         ctypes.POINTER(ctypes.c_double), ctypes.c_int32,
+                                         ctypes.POINTER(ctypes.c_double), _i64p]),
     "bltc_rank_publish_sizes": (ctypes.c_int, [_vp, ctypes.POINTER(PublishSizes)]),
     "bltc_rank_publish": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "bltc_rank_evaluate": (ctypes.c_int, [_vp, ctypes.POINTER(Params), ctypes.c_int32,

@@ -35,7 +35,8 @@ bool launch_moments_bw(const double* sx, const double* sy, const double* sz, con
                        const int32_t* cstop, const double* lo, const double* hi,
                        const double* s_nodes, const double* w_nodes, int degree, int mstride,
                        double* rows, DBuf<int32_t>& cnt, DBuf<int32_t>& off, DBuf<int2>& items,
-                       DBuf<int32_t>& scan_tmp, HostScratch& hs, cudaStream_t st);
+                       DBuf<int32_t>& scan_tmp, HostScratch& hs, cudaStream_t st,
+                       const BwStreams& aux);
 __global__ void k_lists(int64_t nb, int G, int g, const double* bcenter, const double* bradius,
                         const int32_t* bstart, const int32_t* bstop, const MacNode* nodes,
                         int32_t cluster_offset, double theta, int64_t per_node, bool fill,
@@ -120,9 +121,11 @@ __global__ void k_batches(int64_t nb, const int32_t* leaves, const double* lo, c
 // accept geometrically -- a batch ball centred in the domain accepts cluster
 // c only if r_B + r_C <= theta |B - C| (engine.py:65-85), so |B - C| >=
 // r_C / theta must be reachable inside the domain (dom = nullptr: no filter).
+// The domain is a union of n_dom boxes (every batch centre lies in one): the
+// cluster keeps its row if r_C / theta is reachable inside any of them.
 __global__ void k_flag_moments(int64_t nn, const MacNode* nodes, int64_t per_node, int all,
                                const int32_t* used, int32_t* flag, const double* dom,
-                               double theta) {
+                               int64_t n_dom, double theta) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nn) return;
   int f;
@@ -133,14 +136,20 @@ __global__ void k_flag_moments(int64_t nn, const MacNode* nodes, int64_t per_nod
     f = m.eligible && per_node < m.count;                   // any possible approx
     if (f && dom) {
       const double c[3] = {m.cx, m.cy, m.cz};
-      double far2 = 0.0;
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const double e = fmax(fabs(dom[d] - c[d]), fabs(dom[3 + d] - c[d]));
-        far2 += e * e;
-      }
       // generous margins: a cluster on the edge of reach keeps its row
-      f = sqrt(far2) * (1.0 + 1e-9) * theta >= m.radius * (1.0 - 1e-9);
+      const double reach = m.radius * (1.0 - 1e-9) / (theta * (1.0 + 1e-9));
+      const double reach2 = reach * reach;
+      f = 0;
+      for (int64_t k = 0; k < n_dom && !f; ++k) {
+        const double* b = dom + 6 * k;
+        double far2 = 0.0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const double e = fmax(fabs(b[d] - c[d]), fabs(b[3 + d] - c[d]));
+          far2 += e * e;
+        }
+        f = far2 >= reach2;
+      }
     }
   } else {
     f = used[i];
@@ -253,10 +262,12 @@ struct bltc_ctx {
   int device = 0;
   cudaStream_t st = nullptr;
   bool own_stream = false;
+  BwStreams bw;   // the bitwise upward pass's auxiliary stream (created on first use)
   // bltc_rank_set_domain: the global domain, to skip moment rows no batch
   // anywhere could read
-  bool has_domain = false;
-  double domain[6] = {0, 0, 0, 0, 0, 0};
+  // (bltc_rank_set_domain_boxes: a union of boxes, 6 doubles each; empty: unset)
+  std::vector<double> domain;
+  bool domain_uploaded = false;
   DBuf<double> domain_dev;
   bool timing = true;
   HostScratch hs;
@@ -493,9 +504,14 @@ void run_moments(bltc_ctx* c, const bltc_params* p, const double* x, const doubl
                          c->items, c->partial, c->bs.scan_tmp, c->hs, st);
     return;
   }
+  if (!c->bw.st) {
+    BLTC_CUDA(cudaStreamCreateWithFlags(&c->bw.st, cudaStreamNonBlocking));
+    BLTC_CUDA(cudaEventCreateWithFlags(&c->bw.fork, cudaEventDisableTiming));
+    BLTC_CUDA(cudaEventCreateWithFlags(&c->bw.join, cudaEventDisableTiming));
+  }
   if (launch_moments_bw(x, y, z, q, list, n_list, start, stop, lo, hi, c->s_nodes.p,
                         c->w_nodes.p, p->degree, mstride, rows, c->item_cnt, c->item_off,
-                        c->items, c->bs.scan_tmp, c->hs, st))
+                        c->items, c->bs.scan_tmp, c->hs, st, c->bw))
     return;
   const int m = p->degree + 1;
   int threads = ((m * m + 31) / 32) * 32;
@@ -545,14 +561,18 @@ void compute_moments(bltc_ctx* c, const bltc_params* p, const Partition& T, cons
   }
   (void)cluster_base;
   const double* dom = nullptr;
-  if (all == 2 && c->has_domain) {
-    c->domain_dev.resize(6);
-    BLTC_CUDA(cudaMemcpyAsync(c->domain_dev.p, c->domain, 6 * sizeof(double),
-                              cudaMemcpyHostToDevice, st));
+  const int64_t n_dom = (int64_t)(c->domain.size() / 6);
+  if (all == 2 && n_dom > 0) {
+    if (!c->domain_uploaded) {
+      c->domain_dev.resize(c->domain.size());
+      BLTC_CUDA(cudaMemcpyAsync(c->domain_dev.p, c->domain.data(),
+                                c->domain.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+      c->domain_uploaded = true;
+    }
     dom = c->domain_dev.p;
   }
   k_flag_moments<<<grid_for(nn, 256), 256, 0, st>>>(nn, mac, m3, all, c->used.p, c->mflag.p, dom,
-                                                    p->theta);
+                                                    n_dom, p->theta);
   BLTC_LAUNCH_CHECK();
   BLTC_CUDA(cudaMemsetAsync(c->mflag.p + nn, 0, sizeof(int32_t), st));
   exclusive_scan_i32(c->mflag.p, c->mpos.p, nn + 1, c->bs.scan_tmp, st);
@@ -1020,6 +1040,11 @@ int bltc_destroy(bltc_ctx* c) {
     c->f_src4.release();
     c->hs.release();
     c->domain_dev.release();
+    if (c->bw.st) {
+      cudaStreamDestroy(c->bw.st);
+      cudaEventDestroy(c->bw.fork);
+      cudaEventDestroy(c->bw.join);
+    }
     if (c->own_stream) cudaStreamDestroy(c->st);
     delete c;
   });
@@ -1356,22 +1381,75 @@ int bltc_rank_build(bltc_ctx* c, const bltc_params* p, const double* cheb_s, int
   });
 }
 
-int bltc_rank_set_domain(bltc_ctx* c, const double* lo, const double* hi) {
+int bltc_rank_set_domain_boxes(bltc_ctx* c, int64_t n_boxes, const double* boxes) {
   return guarded([&] {
-    if (!c) throw UserError{BLTC_ERR_VALUE};
-    if (!lo || !hi) {
-      c->has_domain = false;
-      return;
-    }
+    if (!c || n_boxes < 0 || (n_boxes > 0 && !boxes)) throw UserError{BLTC_ERR_VALUE};
+    for (int64_t k = 0; k < n_boxes; ++k)
+      for (int d = 0; d < 3; ++d) {
+        const double lo = boxes[6 * k + d], hi = boxes[6 * k + 3 + d];
+        if (!std::isfinite(lo) || !std::isfinite(hi) || lo > hi) {
+          set_error("domain boxes must be finite with lo <= hi");
+          throw UserError{BLTC_ERR_VALUE};
+        }
+      }
+    c->domain.assign(boxes, boxes + 6 * n_boxes);
+    c->domain_uploaded = false;
+  });
+}
+
+int bltc_rank_set_domain(bltc_ctx* c, const double* lo, const double* hi) {
+  if (!lo || !hi) return bltc_rank_set_domain_boxes(c, 0, nullptr);
+  const double box[6] = {lo[0], lo[1], lo[2], hi[0], hi[1], hi[2]};
+  return bltc_rank_set_domain_boxes(c, 1, box);
+}
+
+int bltc_domain_cells(int64_t n, const double* x, const double* y, const double* z, int32_t grid,
+                      double* boxes, int64_t* n_boxes) {
+  return guarded([&] {
+    if (n < 1 || !x || !y || !z || grid < 1 || grid > 64 || !boxes || !n_boxes)
+      throw UserError{BLTC_ERR_VALUE};
+    const double* P[3] = {x, y, z};
+    double lo[3], hi[3];
     for (int d = 0; d < 3; ++d) {
-      if (!std::isfinite(lo[d]) || !std::isfinite(hi[d]) || lo[d] > hi[d]) {
-        set_error("domain bounds must be finite with lo <= hi");
+      lo[d] = hi[d] = P[d][0];
+      for (int64_t i = 1; i < n; ++i) {
+        lo[d] = std::min(lo[d], P[d][i]);
+        hi[d] = std::max(hi[d], P[d][i]);
+      }
+      if (!std::isfinite(lo[d]) || !std::isfinite(hi[d])) {
+        set_error("coordinates must be finite");
         throw UserError{BLTC_ERR_VALUE};
       }
-      c->domain[d] = lo[d];
-      c->domain[3 + d] = hi[d];
     }
-    c->has_domain = true;
+    const int64_t G = grid, nc = G * G * G;
+    std::vector<double> cb(6 * nc);
+    std::vector<char> occ(nc, 0);
+    for (int64_t i = 0; i < n; ++i) {
+      int64_t cell = 0;
+      for (int d = 0; d < 3; ++d) {
+        const double w = hi[d] - lo[d];
+        int64_t k = w > 0 ? (int64_t)((P[d][i] - lo[d]) / w * G) : 0;
+        k = std::min<int64_t>(std::max<int64_t>(k, 0), G - 1);
+        cell = cell * G + k;
+      }
+      double* b = &cb[6 * cell];
+      if (!occ[cell]) {
+        occ[cell] = 1;
+        for (int d = 0; d < 3; ++d) b[d] = b[3 + d] = P[d][i];
+      } else {
+        for (int d = 0; d < 3; ++d) {
+          b[d] = std::min(b[d], P[d][i]);
+          b[3 + d] = std::max(b[3 + d], P[d][i]);
+        }
+      }
+    }
+    int64_t m = 0;
+    for (int64_t cell = 0; cell < nc; ++cell)
+      if (occ[cell]) {
+        std::copy(&cb[6 * cell], &cb[6 * cell] + 6, boxes + 6 * m);
+        ++m;
+      }
+    *n_boxes = m;
   });
 }
 

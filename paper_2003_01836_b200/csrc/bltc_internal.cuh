@@ -119,6 +119,13 @@ struct DBuf {
 };
 
 // Pinned host scratch for small readbacks.
+// An auxiliary stream with fork / join events (the bitwise upward pass runs
+// the big clusters' split items on it, concurrent with the small clusters).
+struct BwStreams {
+  cudaStream_t st = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
 struct HostScratch {
   void* p = nullptr;
   size_t cap = 0;

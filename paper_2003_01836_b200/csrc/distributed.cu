@@ -113,22 +113,20 @@ extern "C" BLTC_API int bltc_run_distributed(int32_t ranks, const int32_t* devic
       }
     }
   const int mstride = (((p->degree + 1) * (p->degree + 1) * (p->degree + 1) + 1) & ~1);
-  // the global domain: each rank publishes only the moment rows some batch
-  // in it could read (bltc_rank_set_domain)
-  double dlo[3] = {x[0], y[0], z[0]}, dhi[3] = {x[0], y[0], z[0]};
-  for (int64_t i = 1; i < n; ++i) {
-    dlo[0] = std::min(dlo[0], x[i]);
-    dlo[1] = std::min(dlo[1], y[i]);
-    dlo[2] = std::min(dlo[2], z[i]);
-    dhi[0] = std::max(dhi[0], x[i]);
-    dhi[1] = std::max(dhi[1], y[i]);
-    dhi[2] = std::max(dhi[2], z[i]);
+  // the global target set as the minimal boxes of its occupied cells on a
+  // 16^3 grid: each rank publishes only the moment rows some batch in them
+  // could read (bltc_rank_set_domain_boxes)
+  std::vector<double> dboxes(6 * 16 * 16 * 16);
+  int64_t n_dboxes = 0;
+  {
+    const int drc = bltc_domain_cells(n, x, y, z, 16, dboxes.data(), &n_dboxes);
+    if (drc != BLTC_OK) return drc;
   }
   // build + publish, one thread per rank
   run_ranks(R, [&](RankBufs& b, int) {
     int rc = bltc_create(b.device, nullptr, &b.ctx);
     if (rc != BLTC_OK) return rc;
-    rc = bltc_rank_set_domain(b.ctx, dlo, dhi);
+    rc = bltc_rank_set_domain_boxes(b.ctx, n_dboxes, dboxes.data());
     if (rc != BLTC_OK) return rc;
     rc = bltc_rank_build(b.ctx, p, cheb_s, b.n, b.x.data(), b.y.data(), b.z.data(),
                          b.q.data(), 0);

@@ -296,6 +296,26 @@ def _all_gather_flat(out, buf, ranks: int, group=None):
         _all_gather(list(out.view(ranks, -1).unbind(0)), buf, group=group)
 
 
+def domain_boxes(x, y, z, grid: int = 16) -> np.ndarray:
+    """The global target set as the minimal bounding boxes of the occupied
+    cells of a ``grid``^3 grid over its bounding box ([k, 6]: lo xyz, hi
+    xyz; bltc_domain_cells, host only).  Every batch centre lies in one of
+    them, so a rank skips the moment rows of clusters no batch in any box
+    could accept (bltc_rank_set_domain_boxes) -- on a Plummer sphere the
+    top clusters of each rank, whose reach r_C / theta falls into the empty
+    corners of the bounding box."""
+    import ctypes
+
+    from . import _lib
+    f64 = lambda a: np.ascontiguousarray(a, dtype=np.float64)
+    x, y, z = f64(x), f64(y), f64(z)
+    out = np.empty((grid ** 3, 6), dtype=np.float64)
+    nb = ctypes.c_int64(0)
+    _lib.check(_lib.load().bltc_domain_cells(len(x), _lib.f64p(x), _lib.f64p(y), _lib.f64p(z),
+                                             grid, _lib.f64p(out), ctypes.byref(nb)))
+    return out[:nb.value].copy()
+
+
 def all_gather_sizes(sizes, ranks: int, group=None, device=None) -> list[tuple]:
     """Every rank's (n_clusters, n_particles, n_moment_rows): one tiny
     all-gather, the step's only host read-back of the exchange."""
@@ -637,13 +657,19 @@ class DeviceRankEngine:
     def set_domain(self, lo, hi) -> None:
         """The bounding box of ALL ranks' targets: moment rows no batch in it
         could read are not computed or published (bltc_rank_set_domain)."""
-        self.domain = (np.asarray(lo, dtype=np.float64), np.asarray(hi, dtype=np.float64))
+        self.set_domain_boxes(np.concatenate([np.asarray(lo, dtype=np.float64),
+                                              np.asarray(hi, dtype=np.float64)]))
+
+    def set_domain_boxes(self, boxes) -> None:
+        """ALL ranks' targets as a union of boxes ([k, 6], e.g. domain_boxes):
+        the tighter form of set_domain (bltc_rank_set_domain_boxes)."""
+        self.domain = np.ascontiguousarray(boxes, dtype=np.float64).reshape(-1, 6)
 
     def build(self, x, y, z, q) -> None:
         torch = self.torch
         dev = torch.device("cuda", self.device)
         dom = getattr(self, "domain", None)
-        self.ctx.rank_set_domain(*(dom if dom is not None else (None, None)))
+        self.ctx.rank_set_domain_boxes(dom if dom is not None else np.empty((0, 6)))
         self._inputs = [torch.as_tensor(np.ascontiguousarray(v, dtype=np.float64)
                                         if not isinstance(v, torch.Tensor) else v,
                                         device=dev).contiguous() for v in (x, y, z, q)]
@@ -826,11 +852,12 @@ def run_distributed(system, config, ranks: int, threads: int = 1, mode: str | No
     x, y, z = np.asarray(src.x), np.asarray(src.y), np.asarray(src.z)
     q = np.asarray(system.charges)
     if len(x):
-        lo = np.array([x.min(), y.min(), z.min()])
-        hi = np.array([x.max(), y.max(), z.max()])
+        boxes = domain_boxes(x, y, z)
         for e in engines.values():
-            if hasattr(e, "set_domain"):
-                e.set_domain(lo, hi)
+            if hasattr(e, "set_domain_boxes"):
+                e.set_domain_boxes(boxes)
+            elif hasattr(e, "set_domain"):
+                e.set_domain(boxes[:, :3].min(axis=0), boxes[:, 3:].max(axis=0))
     if on_device:
         dev = torch.device("cuda", torch.cuda.current_device())
         x, y, z, q = (torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(dev)
@@ -938,8 +965,7 @@ class DeviceRankRunner:
         self.inputs = [torch.from_numpy(np.ascontiguousarray(np.asarray(a)[idx])).to(dev)
                        for a in (src.x, src.y, src.z, system.charges)]
         self.engine = DeviceRankEngine(config, mode, context=ctx)
-        sx, sy, sz = (np.asarray(a) for a in (src.x, src.y, src.z))
-        self.engine.set_domain([sx.min(), sy.min(), sz.min()], [sx.max(), sy.max(), sz.max()])
+        self.engine.set_domain_boxes(domain_boxes(src.x, src.y, src.z))
         self.n_local = int(idx.shape[0])
         self.exchange = exchange
         self.phi = None

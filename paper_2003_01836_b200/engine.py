@@ -251,6 +251,12 @@ class Context:
         hi = np.ascontiguousarray(hi, dtype=np.float64)
         _lib.check(self._lib.bltc_rank_set_domain(self.handle, _lib.f64p(lo), _lib.f64p(hi)))
 
+    def rank_set_domain_boxes(self, boxes) -> None:
+        """The global target domain as a union of boxes ([k, 6]: lo xyz, hi
+        xyz; empty: unset) for the next rank_build."""
+        b = np.ascontiguousarray(boxes, dtype=np.float64).reshape(-1, 6)
+        _lib.check(self._lib.bltc_rank_set_domain_boxes(self.handle, b.shape[0], _lib.f64p(b)))
+
     def rank_publish_sizes(self) -> dict:
         ps = _lib.PublishSizes()
         _lib.check(self._lib.bltc_rank_publish_sizes(self.handle, ctypes.byref(ps)))

@@ -276,3 +276,35 @@ def test_gloo_world3_packed_all_gather(tmp_path):
                        join=True, start_method="spawn")
     for r in range(3):
         assert bool(np.load(tmp_path / f"ok{r}.npy")[0])
+
+
+def test_domain_boxes_cover_the_points():
+    """bltc_domain_cells (host): minimal boxes of the occupied cells of a
+    grid over the points' bounding box -- every point lies in one of them,
+    each is inside the bounding box, at most grid^3 of them; a Plummer
+    sphere leaves the bounding box's corners uncovered (what lets a rank skip
+    its top clusters' moment rows)."""
+    from paper_2003_01836_b200 import cli, decomp
+    s = cli.generate_plummer(20000, 3)
+    x, y, z = (np.asarray(a) for a in (s.sources.x, s.sources.y, s.sources.z))
+    for grid in (1, 4, 16):
+        b = decomp.domain_boxes(x, y, z, grid)
+        assert 1 <= len(b) <= grid ** 3
+        assert (b[:, :3] <= b[:, 3:]).all()
+        P = np.stack([x, y, z], 1)
+        lo, hi = P.min(0), P.max(0)
+        assert (b[:, :3] >= lo).all() and (b[:, 3:] <= hi).all()
+        inside = np.zeros(len(x), dtype=bool)
+        for bb in b:
+            inside |= ((P >= bb[:3]) & (P <= bb[3:])).all(1)
+        assert inside.all()
+        if grid == 1:
+            np.testing.assert_array_equal(b[0], np.concatenate([lo, hi]))
+    corner = hi
+    b = decomp.domain_boxes(x, y, z, 16)
+    assert not ((corner >= b[:, :3]) & (corner <= b[:, 3:])).all(1).any()
+    # the degenerate case: identical points, one box of zero extent
+    b = decomp.domain_boxes(np.ones(5), np.ones(5), np.ones(5), 8)
+    np.testing.assert_array_equal(b, [[1, 1, 1, 1, 1, 1]])
+    with pytest.raises(ValueError, match="finite"):
+        decomp.domain_boxes(np.array([np.nan]), np.zeros(1), np.zeros(1))

@@ -89,6 +89,23 @@ def test_structures_and_moments_bit_exact(bltc, ctx, case):
 
 
 @pytest.mark.parametrize("case", ["c1_coulomb", "plummer", "deg8"])
+@pytest.mark.parametrize("big", ["1", "700"])
+def test_split_moments_bit_exact(bltc, case, big, monkeypatch):
+    """The bitwise upward pass's split items (one CTA per k1, the t2 slot
+    holding a[k1] t2 -- the path of clusters above 2^17 sources), forced onto
+    every cluster above ``big`` sources: moments still bitwise the reference."""
+    monkeypatch.setenv("BLTC_BW_BIG", big)
+    g = golden(case)
+    c = bltc.Context(0)
+    c.build(golden_system(g), _config(bltc, g), mode="parity", all_moments=True)
+    ids, rows = c.export_moments()
+    elig = np.nonzero(g["moments_has"])[0]
+    np.testing.assert_array_equal(ids, elig)
+    np.testing.assert_array_equal(rows, g["moments"][elig])
+    c.close()
+
+
+@pytest.mark.parametrize("case", ["c1_coulomb", "plummer", "deg8"])
 def test_build_only_structures_bit_exact(bltc, case):
     """bltc_build: setup + moments without an evaluation, same structures."""
     g = golden(case)

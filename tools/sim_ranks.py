@@ -25,8 +25,8 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 from paper_2003_01836_b200 import engine  # noqa: E402
-from paper_2003_01836_b200.decomp import (DeviceRankEngine, let_assemble, let_plan,  # noqa: E402
-                                          let_serve, rcb_partition)
+from paper_2003_01836_b200.decomp import (DeviceRankEngine, domain_boxes, let_assemble,  # noqa: E402
+                                          let_plan, let_serve, rcb_partition)
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c4")
@@ -57,10 +57,9 @@ for R in map(int, args.ranks.split(",")):
     part = rcb_partition(src, R)
     ctxs = [engine.Context(0) for _ in range(R)]
     engs = [DeviceRankEngine(econf, args.mode, context=ctxs[r]) for r in range(R)]
-    dom_lo = [float(np.min(a)) for a in (src.x, src.y, src.z)]
-    dom_hi = [float(np.max(a)) for a in (src.x, src.y, src.z)]
+    boxes = domain_boxes(src.x, src.y, src.z)
     for e in engs:
-        e.set_domain(dom_lo, dom_hi)
+        e.set_domain_boxes(boxes)
     inputs = []
     for r in range(R):
         idx = part.rank_indices(r)
