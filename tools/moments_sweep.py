@@ -34,8 +34,9 @@ def main():
     for big in ("65536", "262144", "524288"):
         variants.append({"BLTC_BW_BIG": big})
     # (profiles/r2_moments_sweep6_split_*.jsonl also compared split-kernel
-    # configurations, BLTC_BW_SPLIT 1 / 2 / 3 = producers, ring, CTAs per SM
-    # 4 / 8 / 2 (now the default), 4 / 16 / 1, 2 / 8 / 2 against 8 / 16 / 1)
+    # launch configurations through a since-removed switch, "BLTC_BW_SPLIT"
+    # 1 / 2 / 3 = producers, ring slots, CTAs per SM 4 / 8 / 2 (now the
+    # default), 4 / 16 / 1, 2 / 8 / 2, against 8 / 16 / 1 ({})
     for v in variants:
         os.environ.update(v)
         ts = []
