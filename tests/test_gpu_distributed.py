@@ -201,3 +201,38 @@ def test_rank_domain_filter_keeps_results(bltc):
     np.testing.assert_array_equal(out[True], out[False])
     ref, _ = bltc.treecode_potentials(s, cfg, mode="parity")
     np.testing.assert_array_equal(out[True], ref)
+
+
+@pytest.mark.gpu
+def test_rank_domain_cell_boxes(bltc):
+    """bltc_rank_set_domain_boxes with decomp.domain_boxes' occupied-cell
+    boxes: at most the one-box domain's rows; invalid boxes rejected."""
+    from paper_2003_01836_b200 import cli
+    from paper_2003_01836_b200.decomp import DeviceRankEngine, domain_boxes, rcb_partition
+    s = cli.generate_plummer(60_000, 9)
+    src = s.sources
+    cfg = bltc.EvalConfig(theta=0.8, degree=6, leaf_size=500, batch_size=160)
+    boxes = domain_boxes(src.x, src.y, src.z)
+    part = rcb_partition(src, 2)
+    idx = part.rank_indices(0)
+    rows = {}
+    for mode in ("box", "cells"):
+        eng = DeviceRankEngine(cfg, "parity")
+        if mode == "box":
+            eng.set_domain(boxes[:, :3].min(axis=0), boxes[:, 3:].max(axis=0))
+        else:
+            eng.set_domain_boxes(boxes)
+        eng.build(*(np.ascontiguousarray(np.asarray(a)[idx])
+                    for a in (src.x, src.y, src.z, s.charges)))
+        rows[mode] = eng.publish_sizes()[2]
+        eng.ctx.close()
+    assert rows["cells"] <= rows["box"]
+    # (run_distributed passes the cell boxes to every rank: the oracle
+    # comparisons of the distributed tests above run through them)
+    ctx = bltc.Context(0)
+    with pytest.raises(ValueError):
+        ctx.rank_set_domain_boxes(np.array([[0.0, 0.0, 0.0, -1.0, 1.0, 1.0]]))
+    with pytest.raises(ValueError):
+        ctx.rank_set_domain_boxes(np.array([[np.nan, 0.0, 0.0, 1.0, 1.0, 1.0]]))
+    ctx.rank_set_domain_boxes(np.empty((0, 6)))
+    ctx.close()
