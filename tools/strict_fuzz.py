@@ -27,6 +27,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--runs", type=int, default=100)
     ap.add_argument("--seed", type=int, default=2026)
+    ap.add_argument("--max-n", type=int, default=300_000)
     args = ap.parse_args()
     import paper_2003_01836_b200 as bltc
     from paper_2003_01836_b200 import cli
@@ -35,7 +36,7 @@ def main():
     ctx.keep_strict_bounds(True)
     worst_ratio, worst_rel, bad = 0.0, 0.0, 0
     for run in range(args.runs):
-        n = int(rng.integers(20_000, 300_000))
+        n = int(rng.integers(20_000, args.max_n))
         gen = "plummer" if rng.random() < 0.4 else "uniform"
         system = (cli.generate_plummer if gen == "plummer" else cli.generate_particles)(
             n, int(rng.integers(1, 10_000)))
