@@ -1257,7 +1257,7 @@ int bltc_strict_keep_bounds(bltc_ctx* c, int32_t enable) {
 int bltc_export_strict_bounds(bltc_ctx* c, double* bounds_out, double* kc_out) {
   return guarded([&] {
     require_run(c);
-    if (kc_out) *kc_out = strict_kc();
+    if (kc_out) *kc_out = c->strict.kc_used;
     if (c->n_recomputed != -2 || !c->strict.want_bounds || c->rank_built) {
       set_error("no STRICT single-device run with bltc_strict_keep_bounds enabled");
       throw UserError{BLTC_ERR_STATE};

@@ -163,3 +163,18 @@ def test_strict_distributed_ranks(bltc, case, monkeypatch):
     monkeypatch.setenv("BLTC_STRICT_KC", "1e300")
     phi, st = run_distributed(s, _config(bltc, g), ranks=int(g["ranks"]), mode="strict")
     np.testing.assert_array_equal(phi, g["phi"])
+
+
+def test_certificate_constant_by_degree(bltc):
+    """Kc = 4 from degree 3, 16 at degrees 1-2 (where the measured ratios
+    reach 1.87); exported with the bounds."""
+    from paper_2003_01836_b200 import cli
+    s = cli.generate_particles(20_000, 5)
+    ctx = bltc.Context(0)
+    ctx.keep_strict_bounds(True)
+    for deg, kc in ((1, 16.0), (2, 16.0), (3, 4.0), (8, 4.0)):
+        cfg = bltc.EvalConfig(theta=0.7, degree=deg, leaf_size=300, batch_size=100)
+        ctx.treecode(s, cfg, mode="strict")
+        _, got = ctx.export_strict_bounds()
+        assert got == kc
+    ctx.close()

@@ -28,6 +28,9 @@ def main():
     ap.add_argument("--runs", type=int, default=100)
     ap.add_argument("--seed", type=int, default=2026)
     ap.add_argument("--max-n", type=int, default=300_000)
+    ap.add_argument("--large", action="store_true",
+                    help="instead: the fuzz's worst corner (degree 1-2, many terms per "
+                         "target) at 8M and 32M particles")
     args = ap.parse_args()
     import paper_2003_01836_b200 as bltc
     from paper_2003_01836_b200 import cli
@@ -35,17 +38,27 @@ def main():
     ctx = bltc.Context(0)
     ctx.keep_strict_bounds(True)
     worst_ratio, worst_rel, bad = 0.0, 0.0, 0
+    large = [(n, deg, kap, th, lf, bt) for n in (8_000_000, 32_000_000)
+             for deg, kap, th, lf, bt in ((1, 0.0, 0.7, 500, 500), (2, 18.6, 0.42, 200, 64),
+                                          (1, 0.0, 0.42, 200, 64), (2, 0.0, 0.59, 2000, 160))]
+    if args.large:
+        args.runs = len(large)
     for run in range(args.runs):
-        n = int(rng.integers(20_000, args.max_n))
-        gen = "plummer" if rng.random() < 0.4 else "uniform"
-        system = (cli.generate_plummer if gen == "plummer" else cli.generate_particles)(
-            n, int(rng.integers(1, 10_000)))
-        yuk = rng.random() < 0.35
-        kappa = float(np.exp(rng.uniform(np.log(0.05), np.log(20.0)))) if yuk else 0.0
-        deg = int(rng.integers(1, 13))
-        theta = float(rng.uniform(0.35, 0.95))
-        leaf = int(rng.choice([200, 500, 1000, 2000]))
-        batch = int(rng.choice([64, 160, 300, 500, leaf]))
+        if args.large:
+            n, deg, kappa, theta, leaf, batch = large[run]
+            gen, yuk = "uniform", kappa > 0
+            system = cli.generate_particles(n, run + 1)
+        else:
+            n = int(rng.integers(20_000, args.max_n))
+            gen = "plummer" if rng.random() < 0.4 else "uniform"
+            system = (cli.generate_plummer if gen == "plummer" else cli.generate_particles)(
+                n, int(rng.integers(1, 10_000)))
+            yuk = rng.random() < 0.35
+            kappa = float(np.exp(rng.uniform(np.log(0.05), np.log(20.0)))) if yuk else 0.0
+            deg = int(rng.integers(1, 13))
+            theta = float(rng.uniform(0.35, 0.95))
+            leaf = int(rng.choice([200, 500, 1000, 2000]))
+            batch = int(rng.choice([64, 160, 300, 500, leaf]))
         cfg = bltc.EvalConfig(theta=theta, degree=deg, leaf_size=leaf, batch_size=batch,
                               kernel=bltc.yukawa(kappa) if yuk else bltc.coulomb())
         ref, _ = ctx.treecode(system, cfg, mode="parity")
