@@ -20,6 +20,11 @@ timeout 900 python bench.py --mode parity --steps 2 --no-cpu-baseline --no-accur
   > gpurun_out/bench_parity_c4.json 2> gpurun_out/bench_parity_c4.err
 # STRICT certificate calibration: PARITY vs STRICT over all targets, Kc ratio
 timeout 2400 python tools/strict_calibrate.py --configs c1,c2,c3,c4,c5 > gpurun_out/strict.jsonl 2> gpurun_out/strict.err
+# fuzz: PARITY / STRICT / FAST against the oracle on edge cases; the STRICT
+# certificate over random workloads (profiles/r2_*fuzz*.jsonl)
+timeout 1700 python tools/parity_fuzz.py --runs 2000 > gpurun_out/parity_fuzz.jsonl 2> gpurun_out/parity_fuzz.err
+timeout 1500 python tools/strict_fuzz.py --runs 120 > gpurun_out/strict_fuzz.jsonl 2> gpurun_out/strict_fuzz.err
+timeout 2300 python tools/strict_fuzz.py --runs 150 --seed 7 --max-n 2000000 > gpurun_out/strict_fuzz_large.jsonl 2>&1
 # accuracy cost of N_B; unsampled CPU steps anchoring the extrapolated baseline
 timeout 900 python tools/nb_table.py --config c4 --batch-sizes 160,250,500,1000,2000 > gpurun_out/nb_c4.jsonl 2> gpurun_out/nb_c4.err
 for c in c2 c3 c4; do
